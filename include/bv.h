@@ -1,0 +1,160 @@
+/* =============================================================================
+ * bv.h — C ABI of the B200-native block-Vecchia log-likelihood library.
+ *
+ * The library evaluates, for a frozen plan (blocks, block order ζ, neighbour
+ * lists), the block-Vecchia log-likelihood of arXiv 2410.04477:
+ *
+ *   ℓ(θ) = Σ_k −½ (u_k + d_k + l_k log 2π)                 (Alg. 1 l.28-30,
+ *                                                            PAPER.md:631-633)
+ *   u_k = v_kᵀv_k,  d_k = 2 log det L'_k                    (l.26-27, :627-629)
+ *   L'_k L'_kᵀ = Σlk − Σcrossᵀ Σcon⁻¹ Σcross,
+ *   v_k = L'_k⁻¹ (y_B − Σcrossᵀ Σcon⁻¹ y_NN)                (l.16-25, :602-625)
+ *
+ * with Σlk = K(s_B, s_B), Σcon = K(s_NN, s_NN), Σcross = K(s_NN, s_B)
+ * (l.10-15, :593-599) and K the isotropic Matérn of Eq. (7):
+ * C(r) = σ² 2^{1−ν}/Γ(ν) (r/β)^ν K_ν(r/β), θ = (σ², β, ν).  Eq. (4)
+ * is the approximation this evaluates.  Everything runs in
+ * FP64 on the GPU; nothing falls back to the CPU.
+ *
+ * Conventions:
+ *  - every call returns bv_status; no exception crosses the ABI;
+ *  - inputs are borrowed for the duration of the call: bv_setup copies the
+ *    plan to the device and keeps no caller pointer; outputs are caller-owned
+ *    host memory;
+ *  - a handle is not thread-safe; one evaluation runs at a time; bv_loglik is
+ *    synchronous (ℓ is on the host when it returns);
+ *  - canonical order (part of the contract): the points of a block are taken
+ *    in ascending global id; a neighbour set in the order given (the planner
+ *    emits ascending (distance to centroid, id)).  The joint matrix of block
+ *    k is [NN_k ; B_k] in that order.
+ * ========================================================================== */
+#ifndef BV_H_
+#define BV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BV_OK = 0,
+  BV_EINVAL = 2,   /* invalid plan, θ or argument; bv_last_error names the first violation */
+  BV_ENOTPD = 3,   /* a block's joint covariance is not positive definite (Alg. 1 l.17/l.24 POTRF
+                      fails); *loglik = -INFINITY and bv_last_error gives the smallest failing
+                      permuted position k */
+  BV_EIO = 4,
+  BV_ECUDA = 5,    /* CUDA runtime error (message in bv_last_error) */
+  BV_ENCCL = 6,    /* NCCL error */
+  BV_ENOMEM = 7    /* device allocation failed */
+} bv_status;
+
+typedef struct bv_handle bv_handle; /* opaque; owns all device state, stream, CUDA graph, NCCL comm */
+
+/* The frozen plan (Alg. 1 l.4-9 output).  All pointers are
+ * HOST memory, borrowed for the duration of bv_setup. */
+typedef struct {
+  int64_t n;               /* number of points, n ≥ 1 */
+  int32_t d;               /* dimension, 2 or 3 */
+  const double* locs;      /* n*d row-major coordinates, finite */
+  const double* y;         /* n observations, finite, zero-mean model */
+  int32_t bc;              /* block count, 1 ≤ bc ≤ n */
+  const int32_t* block_id; /* n entries in [0, bc); every block non-empty (partition B, Eq. 2) */
+  const int32_t* order;    /* bc entries, a permutation: order[k] = block at position k (ζ, Eq. 3) */
+  const int64_t* nbr_ptr;  /* bc+1 CSR offsets by POSITION k, nbr_ptr[0] = 0, non-decreasing */
+  const int32_t* nbr_idx;  /* global point ids; set k lies in blocks order[0..k-1] only
+                              (PAPER.md:165), no duplicates; may be empty (position 0) */
+} bv_plan;
+
+/* Distribution (optional).  NULL or world == 1 → single GPU `device`.
+ * world > 1: every rank passes the SAME full plan, its own rank, and the same
+ * 128-byte ncclUniqueId (from bv_nccl_unique_id on rank 0, broadcast by the
+ * caller, e.g. through torch.distributed).  Positions are split into
+ * contiguous, cost-balanced ranges; ℓ is reduced with exactly
+ * one ncclAllReduce per evaluation and is bitwise identical on every rank and
+ * for every world size. */
+typedef struct {
+  int32_t device;
+  int32_t rank;
+  int32_t world;
+  const void* nccl_id; /* 128 bytes (ncclUniqueId) or NULL when world == 1 */
+} bv_dist;
+
+/* Library version string (static storage). */
+const char* bv_version(void);
+
+/* Rank 0 creates the NCCL unique id; out128 must hold 128 bytes. */
+bv_status bv_nccl_unique_id(void* out128);
+
+/* Validate the plan, build the device layout (block-contiguous 32-byte point
+ * records, neighbour lists remapped to permuted indices, size buckets, this
+ * rank's position range), upload it, create the NCCL communicator (world > 1)
+ * and capture the per-evaluation CUDA graph.  *out is NULL on failure.
+ * Errors: BV_EINVAL (plan violation, message names the first one in index
+ * order), BV_ECUDA, BV_ENOMEM, BV_ENCCL.  Runs once per plan; not timed
+ * (PAPER.md:411). */
+bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out);
+
+/* ℓ(θ) for θ = (σ², β, ν) (host array of 3 doubles, each finite and > 0).
+ * Closed forms are used when ν is exactly 0.5, 1.5 or 2.5; any other ν takes
+ * the general K_ν path.  Collective when world > 1 (all ranks, identical θ).
+ * Errors: BV_EINVAL (bad θ), BV_ENOTPD (*loglik = -INFINITY), BV_ECUDA,
+ * BV_ENCCL. */
+bv_status bv_loglik(bv_handle* h, const double theta[3], double* loglik);
+
+/* As bv_loglik, and also the per-block log-determinants d_k and quadratic
+ * forms u_k (Alg. 1 l.26-27) for this rank's positions [k_begin, k_end)
+ * (bv_owned_range), written to logdet[k - k_begin] / quad[k - k_begin]
+ * (host arrays of k_end - k_begin doubles; either may be NULL). */
+bv_status bv_loglik_terms(bv_handle* h, const double theta[3], double* loglik, double* logdet, double* quad);
+
+/* This rank's contiguous range of permuted positions. */
+bv_status bv_owned_range(const bv_handle* h, int32_t* k_begin, int32_t* k_end);
+
+/* End-to-end variant (host observations in, ℓ out): copies y (n host
+ * doubles, in global point-id order) to the device inside the call, then
+ * evaluates.  Used to time the whole path with host↔device traffic. */
+bv_status bv_loglik_host_y(bv_handle* h, const double* y, const double theta[3], double* loglik);
+
+/* Last error message and (after BV_ENOTPD) the smallest failing position, or
+ * -1.  *msg points into the handle and is valid until the next call. */
+bv_status bv_last_error(const bv_handle* h, int32_t* failed_position, const char** msg);
+
+/* The handle's CUDA stream (a cudaStream_t), so a caller can record timing
+ * events on the stream the library's kernels run on. */
+void* bv_stream(const bv_handle* h);
+
+/* Device time (ms) of the block kernels (all size buckets, gather through
+ * per-block terms; excludes θ upload, reduction and allreduce) in the most
+ * recent evaluation, from CUDA events captured inside the graph. */
+bv_status bv_last_kernel_ms(const bv_handle* h, float* ms);
+
+/* Kernel launches per evaluation on this rank (for the bench's gpu_launches). */
+int32_t bv_launches_per_eval(const bv_handle* h);
+
+/* Free everything the handle owns.  NULL is a no-op. */
+void bv_destroy(bv_handle* h);
+
+/* ---- host-side twins, callable without a GPU (tests / multi-rank logic) ---- */
+
+/* Cost-balanced contiguous partition of positions 0..bc-1 over `world`
+ * ranks: cost_k = N_k³/3 + 40·E_k with N_k = m_k + l_k and
+ * E_k = N_k(N_k+1)/2; cut g is the first k with prefix(k) ≥ g·total/world.
+ * l, m: bc entries each.  cuts: world+1 entries (cuts[0] = 0, cuts[world] = bc). */
+bv_status bv_partition(int32_t bc, const int32_t* l, const int32_t* m, int32_t world, int32_t* cuts);
+
+/* Exact fixed-point encoding of a block term t: round(t·2⁶⁴) as
+ * a 192-bit two's-complement integer split into six 32-bit chunks (chunk 0
+ * least significant).  Returns BV_EINVAL for non-finite t or |t| ≥ 2⁹⁶ (so that
+ * up to 2³¹ terms sum without overflowing 192 bits). */
+bv_status bv_fixed_encode(double t, uint32_t chunks[6]);
+
+/* Decode six chunk SUMS (each the sum of up to 2³¹ chunks) to the double
+ * nearest Σ round(t_k·2⁶⁴)·2⁻⁶⁴. */
+double bv_fixed_decode(const uint64_t acc[6]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BV_H_ */

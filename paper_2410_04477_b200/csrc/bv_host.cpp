@@ -1,0 +1,594 @@
+// bv_host.cpp — host runtime behind include/bv.h.
+//
+// bv_setup: validates the frozen plan (Alg. 1 l.4-9 output),
+// lays it out on the device (block-contiguous 32-byte point records, neighbour
+// lists remapped to permuted indices), splits positions across ranks by
+// estimated cost, groups this rank's blocks into size buckets, creates the
+// NCCL communicator and captures ONE CUDA graph per handle:
+//   memcpy θ → bucket kernels (Alg. 1 l.10-29 fused per block) → exact
+//   reduction (l.28-30) → [ncclAllReduce of 7 uint64] → memcpy result.
+// bv_loglik: fills θ (and ν-only constants) into pinned memory, replays the
+// graph, decodes the exact fixed-point sum.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bv.h"
+#include "bv_common.cuh"
+
+namespace bv {
+size_t v1_smem_bytes(int Nmax);
+cudaError_t prepare_block_v1(int Nmax);
+cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
+                            const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
+                            uint32_t* limbs, int32_t* status);
+cudaError_t launch_reduce(const uint32_t* limbs, const int32_t* status, int nq, int k_begin,
+                          unsigned long long* acc, cudaStream_t s);
+cudaError_t launch_scatter_y(const double* y, const int32_t* perm_of_id, int64_t n, PointRec* pts, cudaStream_t s);
+}  // namespace bv
+
+namespace {
+constexpr int kBucketWidth = 16;
+constexpr size_t kSmemOptin = 232448;  // B200 per-block opt-in shared memory
+
+struct Bucket {
+  int Nmax, count, offset;
+};
+}  // namespace
+
+struct bv_handle {
+  int device = 0, rank = 0, world = 1;
+  int64_t n = 0;
+  int d = 2;
+  int32_t bc = 0, kb = 0, ke = 0, nq = 0;
+  cudaStream_t stream = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  ncclComm_t comm = nullptr;
+  bv::PointRec* d_pts = nullptr;
+  int32_t* d_nbr = nullptr;
+  bv::BlockDesc* d_desc = nullptr;
+  int32_t* d_list = nullptr;
+  bv::Theta* d_theta = nullptr;
+  double* d_u = nullptr;
+  double* d_d = nullptr;
+  uint32_t* d_limbs = nullptr;
+  int32_t* d_status = nullptr;
+  unsigned long long* d_acc = nullptr;
+  unsigned long long* d_min = nullptr;
+  int32_t* d_perm_of_id = nullptr;
+  double* d_y_stage = nullptr;
+  bv::Theta* h_theta = nullptr;            // pinned
+  unsigned long long* h_acc = nullptr;     // pinned
+  cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // around the block kernels (graph event nodes)
+  std::vector<Bucket> buckets;
+  std::string err;
+  int32_t failed_pos = -1;
+};
+
+namespace {
+
+bv_status fail(bv_handle* h, bv_status st, const std::string& msg) {
+  if (h) h->err = msg;
+  return st;
+}
+
+#define BV_CUDA(h, call)                                                                              \
+  do {                                                                                                \
+    cudaError_t e_ = (call);                                                                          \
+    if (e_ != cudaSuccess)                                                                            \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? BV_ENOMEM : BV_ECUDA,                          \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                                \
+  } while (0)
+
+#define BV_NCCL(h, call)                                                                              \
+  do {                                                                                                \
+    ncclResult_t r_ = (call);                                                                         \
+    if (r_ != ncclSuccess) return fail(h, BV_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+thread_local std::string g_setup_err;
+
+// ν-only constants of the general-ν K_ν evaluator (bessel_k.cuh), computed in
+// long double once per evaluation.
+void fill_general_nu(bv::Theta& t, double nu) {
+  const long double ln = (long double)nu;
+  const long double nl = std::floor(ln + 0.5L);
+  const long double mu = ln - nl;
+  const long double gampl = 1.0L / std::tgamma(1.0L + mu);
+  const long double gammi = 1.0L / std::tgamma(1.0L - mu);
+  long double gam1;
+  if (std::fabs(mu) >= 1e-3L) {
+    gam1 = (gammi - gampl) / (2.0L * mu);
+  } else {
+    // 1/Γ(1+z) = 1 + γz + c3 z² + c4 z³ + … (Abramowitz–Stegun 6.1.34):
+    // γ1(z) = −(γ + c4 z² + c6 z⁴ + …)
+    const long double g = 0.5772156649015328606065120900824024L;
+    const long double c4 = -0.0420026350340952355290039348754298L;
+    const long double c6 = -0.0421977345555443367482083012891874L;
+    const long double z2 = mu * mu;
+    gam1 = -(g + c4 * z2 + c6 * z2 * z2);
+  }
+  const long double gam2 = 0.5L * (gammi + gampl);
+  const long double pimu = 3.14159265358979323846264338327950288L * mu;
+  const long double fact = (std::fabs(pimu) < 1e-18L) ? 1.0L : pimu / std::sin(pimu);
+  for (double& g : t.gen) g = 0.0;
+  t.gen[0] = (double)mu;
+  t.gen[1] = (double)nl;
+  t.gen[2] = (double)gam1;
+  t.gen[3] = (double)gam2;
+  t.gen[4] = (double)gampl;
+  t.gen[5] = (double)gammi;
+  t.gen[6] = (double)fact;
+}
+
+bool theta_valid(const double* th) {
+  for (int i = 0; i < 3; ++i)
+    if (!(th[i] > 0.0) || !std::isfinite(th[i])) return false;
+  return true;
+}
+
+void fill_theta(bv::Theta& t, const double* th) {
+  std::memset(&t, 0, sizeof(t));
+  t.sigma2 = th[0];
+  t.inv_beta = 1.0 / th[1];
+  t.nu = th[2];
+  if (th[2] == 0.5) t.kind = bv::kNuHalf;
+  else if (th[2] == 1.5) t.kind = bv::kNu3Half;
+  else if (th[2] == 2.5) t.kind = bv::kNu5Half;
+  else {
+    t.kind = bv::kNuGeneral;
+    const long double ln = (long double)th[2];
+    t.c_nu = (double)((long double)th[0] * std::pow(2.0L, 1.0L - ln) / std::tgamma(ln));
+    fill_general_nu(t, th[2]);
+  }
+}
+
+void release(bv_handle* h) {
+  if (!h) return;
+  if (h->device >= 0) cudaSetDevice(h->device);
+  if (h->exec) cudaGraphExecDestroy(h->exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  if (h->comm) ncclCommDestroy(h->comm);
+  void* dev[] = {h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d, h->d_limbs,
+                 h->d_status, h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (h->h_theta) cudaFreeHost(h->h_theta);
+  if (h->h_acc) cudaFreeHost(h->h_acc);
+  if (h->ev_k0) cudaEventDestroy(h->ev_k0);
+  if (h->ev_k1) cudaEventDestroy(h->ev_k1);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  h->exec = nullptr;
+  h->graph = nullptr;
+  h->comm = nullptr;
+}
+
+template <class T>
+bv_status upload(bv_handle* h, T** dst, const T* src, size_t count) {
+  if (count == 0) count = 1;
+  BV_CUDA(h, cudaMalloc((void**)dst, count * sizeof(T)));
+  if (src) BV_CUDA(h, cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  return BV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bv_version(void) { return "bvecchia-b200 0.1 (sm_100a, FP64)"; }
+
+bv_status bv_nccl_unique_id(void* out128) {
+  if (!out128) return BV_EINVAL;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return BV_ENCCL;
+  std::memcpy(out128, &id, sizeof(id));
+  return BV_OK;
+}
+
+bv_status bv_partition(int32_t bc, const int32_t* l, const int32_t* m, int32_t world, int32_t* cuts) {
+  if (bc < 1 || world < 1 || !l || !m || !cuts) return BV_EINVAL;
+  std::vector<double> prefix((size_t)bc + 1, 0.0);
+  for (int32_t k = 0; k < bc; ++k) {
+    const double N = (double)l[k] + (double)m[k];
+    const double cost = N * N * N / 3.0 + 40.0 * (N * (N + 1.0) / 2.0);
+    prefix[(size_t)k + 1] = prefix[k] + cost;
+  }
+  const double total = prefix[bc];
+  cuts[0] = 0;
+  int32_t k = 0;
+  for (int32_t g = 1; g < world; ++g) {
+    const double target = (double)g * total / (double)world;
+    while (k < bc && prefix[k] < target) ++k;
+    cuts[g] = k;
+  }
+  cuts[world] = bc;
+  return BV_OK;
+}
+
+bv_status bv_fixed_encode(double t, uint32_t chunks[6]) {
+  if (!chunks) return BV_EINVAL;
+  return bv::fixed_encode(t, chunks) ? BV_EINVAL : BV_OK;
+}
+
+double bv_fixed_decode(const uint64_t acc[6]) {
+  // Σ acc[c]·2^(32c) mod 2^192, as signed, times 2⁻⁶⁴
+  unsigned __int128 carry = 0;
+  uint64_t L[3];
+  for (int w = 0; w < 3; ++w) {
+    unsigned __int128 s = carry + (unsigned __int128)acc[2 * w] + ((unsigned __int128)acc[2 * w + 1] << 32);
+    L[w] = (uint64_t)s;
+    carry = s >> 64;
+  }
+  const bool neg = (L[2] >> 63) != 0;
+  if (neg) {
+    L[0] = ~L[0]; L[1] = ~L[1]; L[2] = ~L[2];
+    L[0] += 1;
+    if (L[0] == 0) { L[1] += 1; if (L[1] == 0) L[2] += 1; }
+  }
+  // correctly rounded: keep the top 63 significant bits with a sticky bit
+  // (round-to-odd), then one rounding to double
+  int top = -1;
+  for (int w = 2; w >= 0 && top < 0; --w)
+    if (L[w]) top = 64 * w + 63 - __builtin_clzll(L[w]);
+  if (top < 0) return 0.0;
+  auto bit_range = [&](int lo, int nbits) -> uint64_t {  // bits [lo, lo+nbits) of the 192-bit value
+    uint64_t v = 0;
+    for (int b = 0; b < nbits; ++b) {
+      const int p = lo + b;
+      if (p >= 0 && p < 192 && ((L[p >> 6] >> (p & 63)) & 1ull)) v |= (1ull << b);
+    }
+    return v;
+  };
+  const int lo = top - 62;  // 63 bits [lo, top]
+  uint64_t mant = bit_range(lo, 63);
+  if (lo > 0) {
+    bool sticky = false;
+    for (int p = 0; p < lo && !sticky; ++p) sticky = (L[p >> 6] >> (p & 63)) & 1ull;
+    if (sticky) mant |= 1ull;
+  }
+  const double r = std::ldexp((double)mant, lo - 64);  // (double)mant rounds once (63 → 53 bits)
+  return neg ? -r : r;
+}
+
+bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
+  if (!out) return BV_EINVAL;
+  *out = nullptr;
+  bv_handle* h = nullptr;
+  if (!plan) {
+    g_setup_err = "plan is NULL";
+    return BV_EINVAL;
+  }
+  const int64_t n = plan->n;
+  const int d = plan->d;
+  const int32_t bc = plan->bc;
+  auto bad = [&](const std::string& m) {
+    g_setup_err = m;
+    return BV_EINVAL;
+  };
+  if (n < 1 || n > INT32_MAX) return bad("n must be in [1, 2^31)");
+  if (d != 2 && d != 3) return bad("d must be 2 or 3");
+  if (bc < 1 || (int64_t)bc > n) return bad("bc must be in [1, n]");
+  if (!plan->locs || !plan->y || !plan->block_id || !plan->order || !plan->nbr_ptr)
+    return bad("NULL plan array");
+  for (int64_t i = 0; i < n * d; ++i)
+    if (!std::isfinite(plan->locs[i])) return bad("locs[" + std::to_string(i) + "] is not finite");
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(plan->y[i])) return bad("y[" + std::to_string(i) + "] is not finite");
+  std::vector<int64_t> bptr((size_t)bc + 1, 0);
+  for (int64_t i = 0; i < n; ++i) {
+    const int32_t b = plan->block_id[i];
+    if (b < 0 || b >= bc) return bad("block_id[" + std::to_string(i) + "] out of range");
+    bptr[(size_t)b + 1]++;
+  }
+  for (int32_t b = 0; b < bc; ++b)
+    if (bptr[(size_t)b + 1] == 0) return bad("block " + std::to_string(b) + " is empty");
+  for (int32_t b = 0; b < bc; ++b) bptr[(size_t)b + 1] += bptr[b];
+  std::vector<int32_t> pos_of_block(bc, -1);
+  for (int32_t k = 0; k < bc; ++k) {
+    const int32_t b = plan->order[k];
+    if (b < 0 || b >= bc || pos_of_block[b] >= 0) return bad("order is not a permutation (position " + std::to_string(k) + ")");
+    pos_of_block[b] = k;
+  }
+  if (plan->nbr_ptr[0] != 0) return bad("nbr_ptr[0] != 0");
+  for (int32_t k = 0; k < bc; ++k)
+    if (plan->nbr_ptr[k + 1] < plan->nbr_ptr[k]) return bad("nbr_ptr decreases at " + std::to_string(k));
+  const int64_t nnz = plan->nbr_ptr[bc];
+  if (nnz > INT32_MAX) return bad("too many neighbour entries (> 2^31)");
+  if (nnz > 0 && !plan->nbr_idx) return bad("nbr_idx is NULL");
+  {
+    std::vector<int32_t> stamp(n, -1);
+    for (int32_t k = 0; k < bc; ++k)
+      for (int64_t q = plan->nbr_ptr[k]; q < plan->nbr_ptr[k + 1]; ++q) {
+        const int32_t id = plan->nbr_idx[q];
+        if (id < 0 || id >= n) return bad("nbr_idx[" + std::to_string(q) + "] out of range");
+        if (pos_of_block[plan->block_id[id]] >= k)
+          return bad("neighbour " + std::to_string(id) + " of position " + std::to_string(k) +
+                     " is not in an earlier block");
+        if (stamp[id] == k) return bad("duplicate neighbour in position " + std::to_string(k));
+        stamp[id] = k;
+      }
+  }
+  // sizes per position
+  std::vector<int32_t> L(bc), M(bc);
+  int Nmax_all = 0;
+  for (int32_t k = 0; k < bc; ++k) {
+    L[k] = (int32_t)(bptr[(size_t)plan->order[k] + 1] - bptr[plan->order[k]]);
+    M[k] = (int32_t)(plan->nbr_ptr[k + 1] - plan->nbr_ptr[k]);
+    Nmax_all = std::max(Nmax_all, L[k] + M[k]);
+  }
+  const int Nlimit = [] {
+    int N = 8;
+    while (bv::v1_smem_bytes(N + 1) <= kSmemOptin) ++N;
+    return N;
+  }();
+  for (int32_t k = 0; k < bc; ++k)
+    if (L[k] + M[k] > Nlimit)
+      return bad("position " + std::to_string(k) + " has m+l = " + std::to_string(L[k] + M[k]) +
+                 " > " + std::to_string(Nlimit) + " (largest joint size this build supports)");
+
+  // distribution
+  int device = 0, rank = 0, world = 1;
+  const void* nid = nullptr;
+  if (dist) {
+    device = dist->device;
+    rank = dist->rank;
+    world = dist->world;
+    nid = dist->nccl_id;
+  }
+  if (world < 1 || rank < 0 || rank >= world) return bad("invalid rank/world");
+  if (world > 1 && !nid) return bad("world > 1 needs an nccl_id");
+
+  h = new bv_handle();
+  h->device = device;
+  h->rank = rank;
+  h->world = world;
+  h->n = n;
+  h->d = d;
+  h->bc = bc;
+  auto bail = [&](bv_status st) {
+    g_setup_err = h->err;
+    release(h);
+    delete h;
+    return st;
+  };
+#define TRY(x)                         \
+  do {                                 \
+    bv_status s_ = (x);                \
+    if (s_ != BV_OK) return bail(s_);  \
+  } while (0)
+#define TRYC(call)                                                                                   \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      h->err = std::string(#call) + ": " + cudaGetErrorString(e_);                                   \
+      return bail(e_ == cudaErrorMemoryAllocation ? BV_ENOMEM : BV_ECUDA);                           \
+    }                                                                                                \
+  } while (0)
+
+  TRYC(cudaSetDevice(device));
+  TRYC(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+
+  // partition (contiguous, cost-balanced)
+  std::vector<int32_t> cuts((size_t)world + 1);
+  bv_partition(bc, L.data(), M.data(), world, cuts.data());
+  h->kb = cuts[rank];
+  h->ke = cuts[(size_t)rank + 1];
+  h->nq = h->ke - h->kb;
+
+  // permuted point records: positions in order, block points in ascending id
+  std::vector<int32_t> bidx(n);
+  {
+    std::vector<int64_t> fill(bptr.begin(), bptr.end() - 1);
+    for (int64_t i = 0; i < n; ++i) bidx[fill[plan->block_id[i]]++] = (int32_t)i;
+  }
+  std::vector<int32_t> pstart((size_t)bc + 1, 0);
+  for (int32_t k = 0; k < bc; ++k) pstart[(size_t)k + 1] = pstart[k] + L[k];
+  std::vector<int32_t> perm_of_id(n);
+  std::vector<bv::PointRec> pts(n);
+  for (int32_t k = 0; k < bc; ++k) {
+    const int32_t b = plan->order[k];
+    for (int32_t a = 0; a < L[k]; ++a) {
+      const int32_t id = bidx[bptr[b] + a];
+      const int32_t p = pstart[k] + a;
+      perm_of_id[id] = p;
+      const double* s = plan->locs + (size_t)id * d;
+      pts[p] = bv::PointRec{s[0], s[1], d == 3 ? s[2] : 0.0, plan->y[id]};
+    }
+  }
+  // this rank's descriptors and remapped neighbour lists
+  const int64_t nb0 = plan->nbr_ptr[h->kb], nb1 = plan->nbr_ptr[h->ke];
+  std::vector<int32_t> nbr((size_t)(nb1 - nb0));
+  for (int64_t q = nb0; q < nb1; ++q) nbr[(size_t)(q - nb0)] = perm_of_id[plan->nbr_idx[q]];
+  std::vector<bv::BlockDesc> desc((size_t)h->nq);
+  for (int32_t q = 0; q < h->nq; ++q) {
+    const int32_t k = h->kb + q;
+    desc[q] = bv::BlockDesc{pstart[k], L[k], M[k], (int32_t)(plan->nbr_ptr[k] - nb0)};
+  }
+  // size buckets: Nmax = ⌈N/16⌉·16, largest first; inside a bucket N descending, then position
+  std::vector<int32_t> list((size_t)h->nq);
+  for (int32_t q = 0; q < h->nq; ++q) list[q] = q;
+  auto Nq = [&](int32_t q) { return desc[q].l + desc[q].m; };
+  auto bkey = [&](int32_t q) { return (Nq(q) + kBucketWidth - 1) / kBucketWidth; };
+  std::stable_sort(list.begin(), list.end(), [&](int32_t a, int32_t b) {
+    if (bkey(a) != bkey(b)) return bkey(a) > bkey(b);
+    if (Nq(a) != Nq(b)) return Nq(a) > Nq(b);
+    return a < b;
+  });
+  int maxN = 8;
+  for (int32_t i = 0; i < h->nq;) {
+    int32_t j = i;
+    while (j < h->nq && bkey(list[j]) == bkey(list[i])) ++j;
+    const int Nb = std::min(Nlimit, bkey(list[i]) * kBucketWidth);
+    h->buckets.push_back(Bucket{Nb, j - i, i});
+    maxN = std::max(maxN, Nb);
+    i = j;
+  }
+
+  TRY(upload(h, &h->d_pts, pts.data(), pts.size()));
+  TRY(upload(h, &h->d_nbr, nbr.data(), nbr.size()));
+  TRY(upload(h, &h->d_desc, desc.data(), desc.size()));
+  TRY(upload(h, &h->d_list, list.data(), list.size()));
+  TRY(upload(h, &h->d_perm_of_id, perm_of_id.data(), perm_of_id.size()));
+  TRY(upload<double>(h, &h->d_y_stage, nullptr, (size_t)n));
+  TRY(upload<bv::Theta>(h, &h->d_theta, nullptr, 1));
+  TRY(upload<double>(h, &h->d_u, nullptr, (size_t)h->nq));
+  TRY(upload<double>(h, &h->d_d, nullptr, (size_t)h->nq));
+  TRY(upload<uint32_t>(h, &h->d_limbs, nullptr, (size_t)h->nq * 6));
+  TRY(upload<int32_t>(h, &h->d_status, nullptr, (size_t)h->nq));
+  TRY(upload<unsigned long long>(h, &h->d_acc, nullptr, bv::kAccSlots));
+  TRY(upload<unsigned long long>(h, &h->d_min, nullptr, 1));
+  TRYC(cudaMallocHost((void**)&h->h_theta, sizeof(bv::Theta)));
+  TRYC(cudaMallocHost((void**)&h->h_acc, sizeof(unsigned long long) * bv::kAccSlots));
+  std::memset(h->h_theta, 0, sizeof(bv::Theta));
+  TRYC(bv::prepare_block_v1(maxN));
+
+  if (world > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nid, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&h->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      h->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      return bail(BV_ENCCL);
+    }
+  }
+
+  TRYC(cudaEventCreate(&h->ev_k0));
+  TRYC(cudaEventCreate(&h->ev_k1));
+  // capture the per-evaluation graph
+  TRYC(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  {
+    cudaError_t e = cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta), cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k0, h->stream, cudaEventRecordExternal);
+    for (const Bucket& b : h->buckets) {
+      if (e != cudaSuccess) break;
+      e = bv::launch_block_v1(b.count, b.Nmax, h->stream, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset,
+                              h->d_theta, h->d_u, h->d_d, h->d_limbs, h->d_status);
+    }
+    if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k1, h->stream, cudaEventRecordExternal);
+    if (e == cudaSuccess) e = bv::launch_reduce(h->d_limbs, h->d_status, h->nq, h->kb, h->d_acc, h->stream);
+    ncclResult_t r = ncclSuccess;
+    if (e == cudaSuccess && world > 1)
+      r = ncclAllReduce(h->d_acc, h->d_acc, 7, ncclUint64, ncclSum, h->comm, h->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(h->h_acc, h->d_acc, sizeof(unsigned long long) * bv::kAccSlots, cudaMemcpyDeviceToHost,
+                          h->stream);
+    cudaError_t e2 = cudaStreamEndCapture(h->stream, &h->graph);
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+      h->err = std::string("graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
+      return bail(BV_ECUDA);
+    }
+    if (r != ncclSuccess) {
+      h->err = std::string("ncclAllReduce (capture): ") + ncclGetErrorString(r);
+      return bail(BV_ENCCL);
+    }
+  }
+  TRYC(cudaGraphInstantiate(&h->exec, h->graph, 0));
+  *out = h;
+  g_setup_err.clear();
+#undef TRY
+#undef TRYC
+  return BV_OK;
+}
+
+static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
+  h->failed_pos = -1;
+  h->err.clear();
+  if (!theta || !loglik) return fail(h, BV_EINVAL, "NULL argument");
+  if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
+  BV_CUDA(h, cudaSetDevice(h->device));
+  fill_theta(*h->h_theta, theta);
+  BV_CUDA(h, cudaGraphLaunch(h->exec, h->stream));
+  BV_CUDA(h, cudaStreamSynchronize(h->stream));
+  const unsigned long long* acc = h->h_acc;
+  if (acc[6] != 0) {
+    unsigned long long mn = acc[7];
+    if (h->world > 1) {
+      BV_CUDA(h, cudaMemcpyAsync(h->d_min, &mn, 8, cudaMemcpyHostToDevice, h->stream));
+      BV_NCCL(h, ncclAllReduce(h->d_min, h->d_min, 1, ncclUint64, ncclMin, h->comm, h->stream));
+      BV_CUDA(h, cudaMemcpyAsync(&mn, h->d_min, 8, cudaMemcpyDeviceToHost, h->stream));
+      BV_CUDA(h, cudaStreamSynchronize(h->stream));
+    }
+    h->failed_pos = (int32_t)(mn >> 8);
+    *loglik = -INFINITY;
+    if ((mn & 0xff) == bv::kNotPD)
+      return fail(h, BV_ENOTPD, "block at position " + std::to_string(h->failed_pos) + " is not positive definite");
+    return fail(h, BV_EINVAL, "block term at position " + std::to_string(h->failed_pos) + " exceeds 2^96");
+  }
+  uint64_t a6[6];
+  for (int i = 0; i < 6; ++i) a6[i] = acc[i];
+  *loglik = bv_fixed_decode(a6);
+  return BV_OK;
+}
+
+bv_status bv_loglik(bv_handle* h, const double theta[3], double* loglik) {
+  if (!h) return BV_EINVAL;
+  return run_eval(h, theta, loglik);
+}
+
+bv_status bv_loglik_terms(bv_handle* h, const double theta[3], double* loglik, double* logdet, double* quad) {
+  if (!h) return BV_EINVAL;
+  bv_status st = run_eval(h, theta, loglik);
+  if (st != BV_OK && st != BV_ENOTPD) return st;
+  if (h->nq > 0) {
+    if (logdet) BV_CUDA(h, cudaMemcpy(logdet, h->d_d, sizeof(double) * h->nq, cudaMemcpyDeviceToHost));
+    if (quad) BV_CUDA(h, cudaMemcpy(quad, h->d_u, sizeof(double) * h->nq, cudaMemcpyDeviceToHost));
+  }
+  return st;
+}
+
+bv_status bv_loglik_host_y(bv_handle* h, const double* y, const double theta[3], double* loglik) {
+  if (!h || !y) return BV_EINVAL;
+  BV_CUDA(h, cudaSetDevice(h->device));
+  BV_CUDA(h, cudaMemcpyAsync(h->d_y_stage, y, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
+  BV_CUDA(h, bv::launch_scatter_y(h->d_y_stage, h->d_perm_of_id, h->n, h->d_pts, h->stream));
+  return run_eval(h, theta, loglik);
+}
+
+bv_status bv_owned_range(const bv_handle* h, int32_t* k_begin, int32_t* k_end) {
+  if (!h || !k_begin || !k_end) return BV_EINVAL;
+  *k_begin = h->kb;
+  *k_end = h->ke;
+  return BV_OK;
+}
+
+bv_status bv_last_error(const bv_handle* h, int32_t* failed_position, const char** msg) {
+  if (!h) {
+    if (msg) *msg = g_setup_err.c_str();
+    if (failed_position) *failed_position = -1;
+    return BV_OK;
+  }
+  if (failed_position) *failed_position = h->failed_pos;
+  if (msg) *msg = h->err.c_str();
+  return BV_OK;
+}
+
+void* bv_stream(const bv_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+bv_status bv_last_kernel_ms(const bv_handle* h, float* ms) {
+  if (!h || !ms) return BV_EINVAL;
+  cudaError_t e = cudaEventElapsedTime(ms, h->ev_k0, h->ev_k1);
+  return e == cudaSuccess ? BV_OK : BV_ECUDA;
+}
+
+int32_t bv_launches_per_eval(const bv_handle* h) {
+  if (!h) return 0;
+  int32_t c = 1;  // reduction
+  for (const Bucket& b : h->buckets)
+    if (b.count > 0) ++c;
+  return c;
+}
+
+void bv_destroy(bv_handle* h) {
+  if (!h) return;
+  release(h);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle (-m gpu).
+
+Same seeded inputs on both sides (bvgen plan + y drawn by the oracle's
+block-Vecchia simulator at θ, so y follows the model — SURVEY §8c P11a).
+Full element-wise comparison at c1, c2 and c3 sizes; at c4 (n = 1M, 3D) the
+whole ℓ plus element-wise terms on sampled position ranges (the densest tail
+and the head), in the launch configuration bench.py times.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import bvgen
+import oracle
+from paper_2410_04477_b200 import BlockVecchia, BVError, NotPositiveDefinite
+from paper_2410_04477_b200 import build as bvbuild
+
+from parity import compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    bvbuild.build()
+
+
+def sim_plan(name, theta, seed_eps=None, **kw):
+    p = bvgen.cached_plan(name, **kw) if not kw or "n" not in kw else bvgen.make_plan(name, **kw)
+    cfg = bvgen.CONFIGS.get(name, {"cfg": 9})["cfg"]
+    eps = bvgen.normal(seed_eps if seed_eps is not None else 100 * cfg + 2, p.n)
+    return p.with_y(oracle.simulate_bv(p, theta, eps))
+
+
+def full_parity(p, theta, label):
+    bv = BlockVecchia(p)
+    ll, d, u = bv.loglik_terms(theta)
+    o64 = oracle.bv_loglik(p, theta)
+    old = oracle.bv_loglik(p, theta, long_double=True)
+    l, _ = p.block_sizes()
+    s = compare(d, u, o64, old, l, ll, o64["loglik"], label)
+    print(label, s)
+    bv.close()
+    return s
+
+
+@pytest.mark.parametrize("theta", [(1.0, 0.078809, 0.5), (1.0, 0.078809, 1.5), (1.0, 0.078809, 2.5),
+                                   (1.3, 0.05, 0.83), (0.8, 0.03, 1.0)])
+def test_c1_full_parity(theta):
+    p = sim_plan("c1", theta)
+    full_parity(p, theta, f"c1 {theta}")
+
+
+@pytest.mark.parametrize("theta", [(1.0, 0.052537, 1.5), (0.9, 0.06, 1.31)])
+def test_c2_full_parity(theta):
+    p = sim_plan("c2", theta)
+    full_parity(p, theta, f"c2 {theta}")
+
+
+@pytest.mark.parametrize("theta", [(1.0, 0.0025, 2.5), (1.0, 0.014290, 2.5)])
+def test_c3_full_parity(theta):
+    """c3 at the strict-graded β=0.0025 and at Table 1 β (κ-aware branch expected)."""
+    p = sim_plan("c3", theta)
+    full_parity(p, theta, f"c3 {theta}")
+
+
+def test_c4_full_size_sampled_parity():
+    """n = 1M 3D (the headline config): whole ℓ vs the FP64 oracle; terms element-wise on
+    the first 500 and the densest last 2000 positions (long-double oracle there)."""
+    theta = (1.0, 0.017512, 1.5)
+    p = sim_plan("c4", theta)
+    bv = BlockVecchia(p)
+    ll, d, u = bv.loglik_terms(theta)
+    o64 = oracle.bv_loglik(p, theta, per_block=True)
+    rel = abs(ll - o64["loglik"]) / abs(o64["loglik"])
+    assert rel <= 1e-9, rel
+    l, _ = p.block_sizes()
+    for a, b in ((0, 500), (p.bc - 2000, p.bc)):
+        old = oracle.bv_loglik(p, theta, long_double=True, k_range=(a, b))
+        sub = {k: o64[k][a:b] for k in ("u", "d", "t")}
+        s = compare(d[a:b], u[a:b], sub, old, l[a:b], label=f"c4[{a}:{b}]")
+        print("c4", a, b, s, "ll rel", rel)
+    # timed theta too (bench.py's), whole ℓ only
+    th2 = (1.0, 0.052537, 1.5)
+    ll2 = bv.loglik(th2)
+    o2 = oracle.bv_loglik(p, th2, per_block=False)["loglik"]
+    assert abs(ll2 - o2) <= 1e-9 * abs(o2)
+    bv.close()
+
+
+# ---------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("n,bc,m,d", [
+    (50, 1, 10, 2),        # one block, no neighbours (m_1 = 0)
+    (40, 40, 6, 2),        # singleton blocks = classic Vecchia
+    (97, 13, 0, 2),        # m = 0 everywhere: independent blocks
+    (333, 17, 45, 3),      # ragged 3D
+    (700, 7, 100, 2),      # large blocks (N ≈ 200)
+    (64, 2, 70, 2),        # second block conditions on all of the first (m > l_1)
+])
+def test_edge_shapes_parity(n, bc, m, d):
+    theta = (1.2, 0.09, 1.5)
+    p = bvgen.make_plan("c4" if d == 3 else "c1", n=n, bc=bc, m=m, d=d, cfg=31)
+    l, mk = p.block_sizes()
+    if (l + mk).max() > 224:
+        pytest.skip("joint size beyond this build's shared-memory limit")
+    p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(3102, n)))
+    full_parity(p, theta, f"edge n={n} bc={bc} m={m} d={d}")
+
+
+def test_single_block_equals_exact_on_gpu():
+    """bc = 1: the GPU ℓ equals Eq. (1) (oracle's dense exact ℓ)."""
+    theta = (1.0, 0.1, 2.5)
+    p = bvgen.make_plan("c1", n=120, bc=1, m=5, cfg=32)
+    p = p.with_y(oracle.simulate_exact(p.locs, theta, bvgen.normal(7, p.n)))
+    ll = BlockVecchia(p).loglik(theta)
+    ex = oracle.exact_loglik(p.locs, p.y, theta, long_double=True)
+    assert abs(ll - ex) <= 1e-10 * abs(ex)
+
+
+def test_not_pd_reports_smallest_position():
+    theta = (1.0, 0.1, 0.5)
+    p = bvgen.make_plan("c1", n=400, bc=16, m=20, cfg=33)
+    locs = p.locs.copy()
+    for k in (9, 4):  # duplicate a point inside the blocks at positions 9 and 4
+        mem = np.where(p.block_id == p.order[k])[0]
+        locs[mem[1]] = locs[mem[0]]
+    q = bvgen.Plan(locs, p.y, p.block_id, p.order, p.nbr_ptr, p.nbr_idx)
+    with pytest.raises(oracle.OracleError) as eo:
+        oracle.bv_loglik(q, theta)
+    with pytest.raises(NotPositiveDefinite) as eg:
+        BlockVecchia(q).loglik(theta)
+    assert eg.value.failed_position == eo.value.failed_position
+    assert eg.value.failed_position <= 4
+
+
+def test_invalid_theta_rejected():
+    p = bvgen.make_plan("c1", n=100, bc=5, m=5, cfg=34)
+    bv = BlockVecchia(p)
+    for th in [(0.0, 0.1, 0.5), (1.0, -1.0, 0.5), (1.0, 0.1, float("nan")), (float("inf"), 0.1, 0.5)]:
+        with pytest.raises(BVError) as e:
+            bv.loglik(th)
+        assert e.value.status == 2
+
+
+# ---------------------------------------------------------------- properties
+def test_determinism_and_host_y_path():
+    theta = (1.0, 0.052537, 1.5)
+    p = sim_plan("c2", theta)
+    bv = BlockVecchia(p)
+    a = bv.loglik(theta)
+    b = bv.loglik((2.0, 0.1, 0.5))
+    c = bv.loglik(theta)
+    assert a == c and a != b
+    assert bv.loglik_host_y(p.y, theta) == a
+    # a different y through the e2e path, then back
+    y2 = p.y * 0.5
+    assert bv.loglik_host_y(y2, theta) != a
+    assert bv.loglik_host_y(p.y, theta) == a
+
+
+def test_gpu_sigma2_and_length_scaling_exact():
+    """Metamorphic pins on the GPU path: σ²×4 → u/4 bitwise;
+    (coords, β)×2^k → (u, d) bitwise."""
+    theta = (1.0, 0.06, 1.5)
+    p = bvgen.make_plan("c1", n=3000, bc=150, m=40, cfg=35)
+    p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(3502, p.n)))
+    _, d1, u1 = BlockVecchia(p).loglik_terms(theta)
+    _, d4, u4 = BlockVecchia(p).loglik_terms((4.0, 0.06, 1.5))
+    assert np.array_equal(u4, u1 / 4)
+    l, _ = p.block_sizes()
+    assert np.all(np.abs(d4 - d1 - 2 * l * math.log(2.0)) <= 1e-13 * (np.abs(d1) + l))
+    q = bvgen.Plan(p.locs * 8.0, p.y, p.block_id, p.order, p.nbr_ptr, p.nbr_idx)
+    _, d8, u8 = BlockVecchia(q).loglik_terms((1.0, 0.48, 1.5))
+    assert np.array_equal(u8, u1) and np.array_equal(d8, d1)
+
+
+def test_generating_model_on_gpu():
+    """u_k = ‖ε_k‖² when y is simulated block-sequentially (construction pin, any size)."""
+    theta = (1.0, 0.078809, 0.5)
+    p = bvgen.make_plan("c1")
+    eps = bvgen.normal(102, p.n)
+    p = p.with_y(oracle.simulate_bv(p, theta, eps))
+    _, d, u = BlockVecchia(p).loglik_terms(theta)
+    e2 = np.array([np.sum(eps[np.where(p.block_id == b)[0]] ** 2) for b in p.order])
+    assert np.max(np.abs(u - e2) / e2) <= 1e-11
