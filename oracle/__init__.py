@@ -68,7 +68,7 @@ def lib():
             L.or_bv_loglik.argtypes = [C.c_int64, C.c_int, _d, _d, C.c_int32, _i32, _i32, _i64, _i32, _d,
                                        C.c_int, C.c_int, C.c_int32, C.c_int32,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
-                                       C.POINTER(C.c_int32)]
+                                       C.POINTER(C.c_int32), C.c_uint32]
             L.or_exact_loglik.restype = C.c_int
             L.or_exact_loglik.argtypes = [C.c_int64, C.c_int, _d, _d, _d, C.c_int, C.POINTER(C.c_double)]
             L.or_classic_vecchia.restype = C.c_int
@@ -129,13 +129,17 @@ def trsv(Lm, b):
     return x
 
 
-def bv_loglik(plan, theta, long_double: bool = False, nthreads: int = 0, k_range=None, per_block: bool = True):
+def bv_loglik(plan, theta, long_double: bool = False, nthreads: int = 0, k_range=None, per_block: bool = True,
+              perturb_seed: int = 0):
     """Alg. 1 literally.  Returns dict(loglik, u, d, t).
 
     ``plan`` carries numpy arrays ``locs (n,d) f64, y (n,) f64, block_id (n,)
     i32, order (bc,) i32, nbr_ptr (bc+1,) i64, nbr_idx (nnz,) i32``.
     ``k_range`` = (k_begin, k_end) restricts to those permuted positions.
     Raises OracleError(3, k) on a non-PD block (k = smallest failing position).
+    ``perturb_seed`` != 0 moves every off-diagonal covariance entry by −1/0/+1
+    ulp (a fixed function of the point pair and the seed): the spread over a
+    few seeds estimates FP64's own error (parity reading G22).
     """
     L = lib()
     locs = _c(plan.locs, np.float64)
@@ -153,7 +157,7 @@ def bv_loglik(plan, theta, long_double: bool = False, nthreads: int = 0, k_range
                         _c(plan.order, np.int32), _c(plan.nbr_ptr, np.int64), _c(plan.nbr_idx, np.int32), th,
                         1 if long_double else 0, int(nthreads), kb, ke,
                         u.ctypes.data if per_block else None, dd.ctypes.data if per_block else None,
-                        t.ctypes.data if per_block else None, C.byref(ll), C.byref(fp))
+                        t.ctypes.data if per_block else None, C.byref(ll), C.byref(fp), int(perturb_seed))
     if st:
         raise OracleError(st, fp.value)
     return {"loglik": ll.value, "u": u, "d": dd, "t": t}

@@ -98,6 +98,27 @@ template <class R> inline R dist(const double* a, const double* b, int d) {
   return std::sqrt(s);
 }
 
+/* Optional ±1-ulp perturbation of a covariance entry (parity reading G22,
+ * DESIGN.md §3): FP64 cannot distinguish Σ from Σ with every entry moved by
+ * one ulp, so the spread of FP64 results over a few such perturbations
+ * estimates FP64's own error at ill-conditioned blocks.  The perturbation of
+ * the pair {a, b} is a fixed function of (min id, max id, seed), so Σcon,
+ * Σcross and Σlk see one consistent symmetric matrix; the diagonal (a == b)
+ * is never perturbed.  seed == 0 → no perturbation (the default oracle). */
+inline double perturb_entry(double v, int32_t a, int32_t b, uint32_t seed) {
+  if (seed == 0 || a == b) return v;
+  uint64_t lo = (uint64_t)(a < b ? a : b), hi = (uint64_t)(a < b ? b : a);
+  uint64_t z = (lo << 32 | hi) + 0x9E3779B97F4A7C15ull * (uint64_t)seed;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  const int r = (int)(z % 3u);
+  if (r == 0) return std::nextafter(v, -INFINITY);
+  if (r == 2) return std::nextafter(v, INFINITY);
+  return v;
+}
+inline long double perturb_entry(long double v, int32_t, int32_t, uint32_t) { return v; }
+
 /* Textbook unblocked Cholesky (Cholesky–Crout, column by column), row-major
  * lower factor in L (n×n, only j ≤ i used).  Returns false on a pivot that is
  * ≤ 0 or not finite (reading: non-PD → failure). */
@@ -152,7 +173,7 @@ void build_block_lists(PlanView& P, const int32_t* block_id) {
 /* One block of Alg. 1, literally, at permuted position k.
  * Returns 0, or 3 if a POTRF failed (non-PD). */
 template <class R>
-int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R* d_out) {
+int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R* d_out, uint32_t seed) {
   const int32_t b = P.order[k];
   const int l = (int)(P.bptr[(size_t)b + 1] - P.bptr[b]);
   const int32_t* B = P.bidx.data() + P.bptr[b];
@@ -164,7 +185,8 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
   // l.11  Σlk ← K(s_B, s_B)          (l×l)
   std::vector<R> Slk((size_t)l * l);
   for (int a = 0; a < l; ++a)
-    for (int c = 0; c < l; ++c) Slk[(size_t)a * l + c] = matern<R>(dist<R>(loc(B[a]), loc(B[c]), d), sigma2, beta, nu);
+    for (int c = 0; c < l; ++c)
+      Slk[(size_t)a * l + c] = perturb_entry(matern<R>(dist<R>(loc(B[a]), loc(B[c]), d), sigma2, beta, nu), B[a], B[c], seed);
   // l.14  y_B, y_NN
   std::vector<R> yB(l), yN(m);
   for (int a = 0; a < l; ++a) yB[a] = R(P.y[B[a]]);
@@ -176,11 +198,13 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
     // l.12  Σcon ← K(s_NN, s_NN)    (m×m)
     std::vector<R> Scon((size_t)m * m);
     for (int a = 0; a < m; ++a)
-      for (int c = 0; c < m; ++c) Scon[(size_t)a * m + c] = matern<R>(dist<R>(loc(NN[a]), loc(NN[c]), d), sigma2, beta, nu);
+      for (int c = 0; c < m; ++c)
+        Scon[(size_t)a * m + c] = perturb_entry(matern<R>(dist<R>(loc(NN[a]), loc(NN[c]), d), sigma2, beta, nu), NN[a], NN[c], seed);
     // l.13  Σcross ← K(s_NN, s_B)   (m×l, reading G8)
     std::vector<R> Scross((size_t)m * l);
     for (int a = 0; a < m; ++a)
-      for (int c = 0; c < l; ++c) Scross[(size_t)a * l + c] = matern<R>(dist<R>(loc(NN[a]), loc(B[c]), d), sigma2, beta, nu);
+      for (int c = 0; c < l; ++c)
+        Scross[(size_t)a * l + c] = perturb_entry(matern<R>(dist<R>(loc(NN[a]), loc(B[c]), d), sigma2, beta, nu), NN[a], B[c], seed);
     // l.17  L ← POTRF(Σcon)
     std::vector<R> L;
     if (!potrf<R>(Scon, L, m)) return 3;
@@ -228,7 +252,7 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
 template <class R>
 int bv_loglik_impl(PlanView& P, const int32_t* block_id, const double* theta, double* out_u, double* out_d,
                    double* out_t, double* out_loglik, int32_t* failed_pos, int nthreads, int k_begin, int k_end,
-                   double* out_loglik_ld_sum) {
+                   double* out_loglik_ld_sum, uint32_t seed) {
   build_block_lists(P, block_id);
   const R sigma2 = R(theta[0]), beta = R(theta[1]), nu = R(theta[2]);
   const int nk = k_end - k_begin;
@@ -241,7 +265,7 @@ int bv_loglik_impl(PlanView& P, const int32_t* block_id, const double* theta, do
   for (int q = 0; q < nk; ++q) {
     const int32_t k = k_begin + q;
     R u = 0, d = 0;
-    st[q] = alg1_block<R>(P, k, sigma2, beta, nu, &u, &d);
+    st[q] = alg1_block<R>(P, k, sigma2, beta, nu, &u, &d, seed);
     const int l = (int)(P.bptr[(size_t)P.order[k] + 1] - P.bptr[P.order[k]]);
     uu[q] = u;
     dd[q] = d;
@@ -338,19 +362,21 @@ void or_trsv(const double* L, int n, double* x) {
  *   theta = (σ², β, ν).  long_double != 0 runs the whole algorithm in 80-bit.
  *   Per-block outputs (u_k, d_k, t_k) for positions [k_begin, k_end) are
  *   written to out_* (each may be NULL); out_loglik = Σ t_k over that range.
+ *   perturb_seed != 0 (FP64 only): every off-diagonal covariance entry moved
+ *   by −1, 0 or +1 ulp (perturb_entry; parity reading G22).
  * Returns 0, 2 (invalid θ) or 3 (non-PD; *failed_pos = smallest failing k). */
 int or_bv_loglik(int64_t n, int d, const double* locs, const double* y, int32_t bc, const int32_t* block_id,
                  const int32_t* order, const int64_t* nbr_ptr, const int32_t* nbr_idx, const double* theta,
                  int long_double, int nthreads, int32_t k_begin, int32_t k_end, double* out_u, double* out_d,
-                 double* out_t, double* out_loglik, int32_t* failed_pos) {
+                 double* out_t, double* out_loglik, int32_t* failed_pos, uint32_t perturb_seed) {
   if (!theta_ok(theta) || n < 1 || (d != 2 && d != 3) || bc < 1 || k_begin < 0 || k_end > bc || k_begin > k_end)
     return 2;
   PlanView P{n, d, locs, y, bc, order, nbr_ptr, nbr_idx, {}, {}};
   if (long_double)
     return bv_loglik_impl<long double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads,
-                                       k_begin, k_end, nullptr);
+                                       k_begin, k_end, nullptr, 0u);
   return bv_loglik_impl<double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads, k_begin,
-                                k_end, nullptr);
+                                k_end, nullptr, perturb_seed);
 }
 
 /* Eq. (1): ℓ = −n/2 log 2π − ½ log|Σθ| − ½ yᵀΣθ⁻¹y, dense

@@ -34,13 +34,18 @@ def sim_plan(name, theta, seed_eps=None, **kw):
     return p.with_y(oracle.simulate_bv(p, theta, eps))
 
 
+def replicas(p, theta, k_range=None):
+    """FP64 oracle runs with ±1-ulp perturbed entries (parity reading G22)."""
+    return [oracle.bv_loglik(p, theta, k_range=k_range, perturb_seed=s) for s in (1, 2, 3)]
+
+
 def full_parity(p, theta, label):
     bv = BlockVecchia(p)
     ll, d, u = bv.loglik_terms(theta)
     o64 = oracle.bv_loglik(p, theta)
     old = oracle.bv_loglik(p, theta, long_double=True)
     l, _ = p.block_sizes()
-    s = compare(d, u, o64, old, l, ll, o64["loglik"], label)
+    s = compare(d, u, o64, old, l, ll, o64["loglik"], label, replicas=replicas(p, theta))
     print(label, s)
     bv.close()
     return s
@@ -80,7 +85,8 @@ def test_c4_full_size_sampled_parity():
     for a, b in ((0, 500), (p.bc - 2000, p.bc)):
         old = oracle.bv_loglik(p, theta, long_double=True, k_range=(a, b))
         sub = {k: o64[k][a:b] for k in ("u", "d", "t")}
-        s = compare(d[a:b], u[a:b], sub, old, l[a:b], label=f"c4[{a}:{b}]")
+        s = compare(d[a:b], u[a:b], sub, old, l[a:b], label=f"c4[{a}:{b}]",
+                    replicas=replicas(p, theta, k_range=(a, b)))
         print("c4", a, b, s, "ll rel", rel)
     # timed theta too (bench.py's), whole ℓ only
     th2 = (1.0, 0.052537, 1.5)

@@ -301,3 +301,20 @@ def test_invalid_theta_rejected():
         with pytest.raises(oracle.OracleError) as e:
             oracle.bv_loglik(p, th)
         assert e.value.status == 2
+
+
+def test_perturbed_replicas_measure_fp64_error_at_high_kappa():
+    """Reading G22: ±1-ulp entry replicas spread by ≈ FP64's own error; well-conditioned
+    blocks barely move (c1, κ ≲ 2e3), and the spread never exceeds the long-double gap by orders."""
+    theta = (1.0, 0.078809, 0.5)
+    p = bvgen.make_plan("c1")
+    p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(102, p.n)))
+    ld = oracle.bv_loglik(p, theta, long_double=True)
+    l, _ = p.block_sizes()
+    s = np.abs(ld["u"]) + np.abs(ld["d"]) + l * oracle.ln_2pi()
+    for seed in (1, 2, 3):
+        r = oracle.bv_loglik(p, theta, perturb_seed=seed)
+        assert np.max(np.abs(r["t"] - ld["t"]) / s) <= 1e-13
+    a = oracle.bv_loglik(p, theta, perturb_seed=1)
+    b = oracle.bv_loglik(p, theta, perturb_seed=1)
+    assert np.array_equal(a["t"], b["t"])  # deterministic
