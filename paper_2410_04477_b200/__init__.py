@@ -22,7 +22,7 @@ __all__ = ["BlockVecchia", "BVError", "NotPositiveDefinite", "lib", "nccl_unique
            "fixed_encode", "fixed_decode", "LIB_PATH"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbv.so")
+LIB_PATH = os.environ.get("BV_LIB_PATH") or os.path.join(HERE, "libbv.so")  # override: debug builds only
 
 BV_OK, BV_EINVAL, BV_ENOTPD, BV_EIO, BV_ECUDA, BV_ENCCL, BV_ENOMEM = 0, 2, 3, 4, 5, 6, 7
 _NAMES = {2: "BV_EINVAL", 3: "BV_ENOTPD", 4: "BV_EIO", 5: "BV_ECUDA", 6: "BV_ENCCL", 7: "BV_ENOMEM"}

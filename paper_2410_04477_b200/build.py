@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbv.so")
-SOURCES = ["bv_host.cpp", "bv_kernels.cu"]
+SOURCES = ["bv_host.cpp", "bv_kernels.cu", "bv_block_v2.cu"]
 HEADERS = ["bv_common.cuh", "matern.cuh", "bessel_k.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -35,20 +35,24 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, profile_phases: bool = False) -> str:
+    """Build libbv.so (or, with profile_phases, the debug-instrumented libbv_prof.so)."""
+    out = LIB if not profile_phases else os.path.join(HERE, "libbv_prof.so")
+    if not profile_phases and not force and not _stale():
         return LIB
     inc, libdir = nccl_dirs()
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = (["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
+    tmp = out + f".tmp{os.getpid()}"
+    extra = ["-DBV_PROFILE_PHASES"] if profile_phases else []
+    cmd = (["nvcc", *ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
             "-Xptxas", "-v" if verbose else "-O3",
             "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc, "-o", tmp]
            + [os.path.join(CSRC, f) for f in SOURCES]
            + ["-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}"])
     subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                profile_phases="--profile-phases" in sys.argv))

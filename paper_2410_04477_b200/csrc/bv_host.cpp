@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -31,6 +32,14 @@ cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRe
 cudaError_t launch_reduce(const uint32_t* limbs, const int32_t* status, int nq, int k_begin,
                           unsigned long long* acc, cudaStream_t s);
 cudaError_t launch_scatter_y(const double* y, const int32_t* perm_of_id, int64_t n, PointRec* pts, cudaStream_t s);
+int v2_maxt_for(int TI);
+int debug_phase_cycles(unsigned long long* out, int reset);
+size_t v2_smem_bytes(int TImax, int cap);
+cudaError_t prepare_block_v2(size_t max_smem);
+cudaError_t launch_block_v2(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
+                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
+                            const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
+                            uint32_t* limbs, int32_t* status);
 }  // namespace bv
 
 namespace {
@@ -38,7 +47,48 @@ constexpr int kBucketWidth = 16;
 constexpr size_t kSmemOptin = 232448;  // B200 per-block opt-in shared memory
 
 struct Bucket {
-  int Nmax, count, offset;
+  int Nmax, count, offset;  // v1: Nmax = joint size bound; v2: Nmax = tile rows TI
+  int cap;                  // v2: L slots for this TI
+};
+
+// L-slot recycling tables for the v2 kernel (bv_block_v2.cu).  For a block
+// with TI tile rows and TJ column panels, tile L(I,K) lives from the end of
+// panel K to panel I; row J's tiles are dead once panel J's update has read
+// them, and panel J then writes column J.  Simulate that with a LIFO free
+// list; slot[I·TI + K] is the slot of L(I,K).  off[2·TI + (TI−TJ)] indexes
+// the table of each (TI, TJ) pair (TI − TJ ∈ {0, 1}); cap[TI] = max slots.
+struct SlotTables {
+  std::vector<int16_t> tabs;
+  std::vector<int32_t> off;
+  std::vector<int> cap;
+  void build(int TImax) {
+    off.assign(2 * (size_t)(TImax + 1), 0);
+    cap.assign((size_t)TImax + 1, 0);
+    tabs.clear();
+    for (int TI = 1; TI <= TImax; ++TI)
+      for (int e = 0; e < 2; ++e) {
+        const int TJ = TI - e;
+        off[2 * TI + e] = (int32_t)tabs.size();
+        std::vector<int16_t> t((size_t)TI * TI, -1);
+        std::vector<int16_t> freel;
+        int next = 0;
+        for (int J = 0; J < TJ; ++J) {
+          for (int K = 0; K < J; ++K) freel.push_back(t[(size_t)J * TI + K]);
+          for (int I = J + 1; I < TI; ++I) {
+            if (!freel.empty()) {
+              t[(size_t)I * TI + J] = freel.back();
+              freel.pop_back();
+            } else {
+              t[(size_t)I * TI + J] = (int16_t)next++;
+            }
+          }
+        }
+        for (auto& v : t)
+          if (v < 0) v = 0;
+        tabs.insert(tabs.end(), t.begin(), t.end());
+        cap[TI] = std::max(cap[TI], std::max(next, 1));
+      }
+  }
 };
 }  // namespace
 
@@ -48,8 +98,8 @@ struct bv_handle {
   int d = 2;
   int32_t bc = 0, kb = 0, ke = 0, nq = 0;
   cudaStream_t stream = nullptr;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph[4] = {nullptr, nullptr, nullptr, nullptr};      // one per MaternKind
+  cudaGraphExec_t exec[4] = {nullptr, nullptr, nullptr, nullptr};
   ncclComm_t comm = nullptr;
   bv::PointRec* d_pts = nullptr;
   int32_t* d_nbr = nullptr;
@@ -64,6 +114,10 @@ struct bv_handle {
   unsigned long long* d_min = nullptr;
   int32_t* d_perm_of_id = nullptr;
   double* d_y_stage = nullptr;
+  int16_t* d_tabs = nullptr;
+  double* d_exptab = nullptr;
+  int32_t* d_tab_off = nullptr;
+  bool use_v1 = false;
   bv::Theta* h_theta = nullptr;            // pinned
   unsigned long long* h_acc = nullptr;     // pinned
   cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // around the block kernels (graph event nodes)
@@ -153,11 +207,15 @@ void fill_theta(bv::Theta& t, const double* th) {
 void release(bv_handle* h) {
   if (!h) return;
   if (h->device >= 0) cudaSetDevice(h->device);
-  if (h->exec) cudaGraphExecDestroy(h->exec);
-  if (h->graph) cudaGraphDestroy(h->graph);
+  for (int k = 0; k < 4; ++k) {
+    if (h->exec[k]) cudaGraphExecDestroy(h->exec[k]);
+    if (h->graph[k]) cudaGraphDestroy(h->graph[k]);
+    h->exec[k] = nullptr;
+    h->graph[k] = nullptr;
+  }
   if (h->comm) ncclCommDestroy(h->comm);
   void* dev[] = {h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d, h->d_limbs,
-                 h->d_status, h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage};
+                 h->d_status, h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (h->h_theta) cudaFreeHost(h->h_theta);
@@ -165,8 +223,6 @@ void release(bv_handle* h) {
   if (h->ev_k0) cudaEventDestroy(h->ev_k0);
   if (h->ev_k1) cudaEventDestroy(h->ev_k1);
   if (h->stream) cudaStreamDestroy(h->stream);
-  h->exec = nullptr;
-  h->graph = nullptr;
   h->comm = nullptr;
 }
 
@@ -323,9 +379,21 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     M[k] = (int32_t)(plan->nbr_ptr[k + 1] - plan->nbr_ptr[k]);
     Nmax_all = std::max(Nmax_all, L[k] + M[k]);
   }
-  const int Nlimit = [] {
+  const char* kenv = std::getenv("BV_KERNEL");
+  const bool use_v1 = kenv && std::string(kenv) == "v1";
+  const int Nlimit = [&] {
     int N = 8;
-    while (bv::v1_smem_bytes(N + 1) <= kSmemOptin) ++N;
+    if (use_v1) {
+      while (bv::v1_smem_bytes(N + 1) <= kSmemOptin) ++N;
+      return N;
+    }
+    SlotTables st;
+    st.build(48);
+    while (N + 1 < 8 * 48) {
+      const int TI = (N + 1 + 8) >> 3;
+      if (bv::v2_smem_bytes(TI, st.cap[TI]) > kSmemOptin || bv::v2_maxt_for(TI) < 0) break;
+      ++N;
+    }
     return N;
   }();
   for (int32_t k = 0; k < bc; ++k)
@@ -352,6 +420,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   h->n = n;
   h->d = d;
   h->bc = bc;
+  h->use_v1 = use_v1;
   auto bail = [&](bv_status st) {
     g_setup_err = h->err;
     release(h);
@@ -411,23 +480,35 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     const int32_t k = h->kb + q;
     desc[q] = bv::BlockDesc{pstart[k], L[k], M[k], (int32_t)(plan->nbr_ptr[k] - nb0)};
   }
-  // size buckets: Nmax = ⌈N/16⌉·16, largest first; inside a bucket N descending, then position
+  // size buckets, largest first; inside a bucket N descending, then position.
+  //   v2: one bucket per tile-row count TI = ⌈(N+1)/8⌉;  v1: N rounded up to 16.
   std::vector<int32_t> list((size_t)h->nq);
   for (int32_t q = 0; q < h->nq; ++q) list[q] = q;
   auto Nq = [&](int32_t q) { return desc[q].l + desc[q].m; };
-  auto bkey = [&](int32_t q) { return (Nq(q) + kBucketWidth - 1) / kBucketWidth; };
+  auto bkey = [&](int32_t q) { return use_v1 ? (Nq(q) + kBucketWidth - 1) / kBucketWidth : (Nq(q) + 8) >> 3; };
   std::stable_sort(list.begin(), list.end(), [&](int32_t a, int32_t b) {
     if (bkey(a) != bkey(b)) return bkey(a) > bkey(b);
     if (Nq(a) != Nq(b)) return Nq(a) > Nq(b);
     return a < b;
   });
+  SlotTables slot_tables;
+  int TImax_all = 1;
+  for (int32_t q = 0; q < h->nq; ++q) TImax_all = std::max(TImax_all, (Nq(q) + 8) >> 3);
+  slot_tables.build(TImax_all);
   int maxN = 8;
+  size_t max_smem = 0;
   for (int32_t i = 0; i < h->nq;) {
     int32_t j = i;
     while (j < h->nq && bkey(list[j]) == bkey(list[i])) ++j;
-    const int Nb = std::min(Nlimit, bkey(list[i]) * kBucketWidth);
-    h->buckets.push_back(Bucket{Nb, j - i, i});
-    maxN = std::max(maxN, Nb);
+    if (use_v1) {
+      const int Nb = std::min(Nlimit, bkey(list[i]) * kBucketWidth);
+      h->buckets.push_back(Bucket{Nb, j - i, i, 0});
+      maxN = std::max(maxN, Nb);
+    } else {
+      const int TI = bkey(list[i]);
+      h->buckets.push_back(Bucket{TI, j - i, i, slot_tables.cap[TI]});
+      max_smem = std::max(max_smem, bv::v2_smem_bytes(TI, slot_tables.cap[TI]));
+    }
     i = j;
   }
 
@@ -447,7 +528,15 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   TRYC(cudaMallocHost((void**)&h->h_theta, sizeof(bv::Theta)));
   TRYC(cudaMallocHost((void**)&h->h_acc, sizeof(unsigned long long) * bv::kAccSlots));
   std::memset(h->h_theta, 0, sizeof(bv::Theta));
-  TRYC(bv::prepare_block_v1(maxN));
+  TRY(upload(h, &h->d_tabs, slot_tables.tabs.data(), slot_tables.tabs.size()));
+  TRY(upload(h, &h->d_tab_off, slot_tables.off.data(), slot_tables.off.size()));
+  {
+    double et[64];  // 2^{−j/64}, correctly rounded via long double (exp_neg in matern.cuh)
+    for (int j = 0; j < 64; ++j) et[j] = (double)std::exp2(-(long double)j / 64.0L);
+    TRY(upload(h, &h->d_exptab, et, 64));
+  }
+  if (use_v1) TRYC(bv::prepare_block_v1(maxN));
+  else TRYC(bv::prepare_block_v2(std::max<size_t>(max_smem, 1024)));
 
   if (world > 1) {
     ncclUniqueId id;
@@ -461,15 +550,21 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
 
   TRYC(cudaEventCreate(&h->ev_k0));
   TRYC(cudaEventCreate(&h->ev_k1));
-  // capture the per-evaluation graph
-  TRYC(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-  {
+  // capture the per-evaluation graph, one per Matérn kind (the block kernel is
+  // specialised on it; the kind is chosen from ν at each evaluation)
+  for (int kind = 0; kind < 4; ++kind) {
+    TRYC(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t e = cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta), cudaMemcpyHostToDevice, h->stream);
     if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k0, h->stream, cudaEventRecordExternal);
     for (const Bucket& b : h->buckets) {
       if (e != cudaSuccess) break;
-      e = bv::launch_block_v1(b.count, b.Nmax, h->stream, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset,
-                              h->d_theta, h->d_u, h->d_d, h->d_limbs, h->d_status);
+      if (use_v1)
+        e = bv::launch_block_v1(b.count, b.Nmax, h->stream, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset,
+                                h->d_theta, h->d_u, h->d_d, h->d_limbs, h->d_status);
+      else
+        e = bv::launch_block_v2(kind, b.count, b.Nmax, b.cap, h->stream, h->d_pts, h->d_nbr, h->d_desc,
+                                h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
+                                h->d_d, h->d_limbs, h->d_status);
     }
     if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k1, h->stream, cudaEventRecordExternal);
     if (e == cudaSuccess) e = bv::launch_reduce(h->d_limbs, h->d_status, h->nq, h->kb, h->d_acc, h->stream);
@@ -479,7 +574,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(h->h_acc, h->d_acc, sizeof(unsigned long long) * bv::kAccSlots, cudaMemcpyDeviceToHost,
                           h->stream);
-    cudaError_t e2 = cudaStreamEndCapture(h->stream, &h->graph);
+    cudaError_t e2 = cudaStreamEndCapture(h->stream, &h->graph[kind]);
     if (e != cudaSuccess || e2 != cudaSuccess) {
       h->err = std::string("graph capture: ") + cudaGetErrorString(e != cudaSuccess ? e : e2);
       return bail(BV_ECUDA);
@@ -488,8 +583,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
       h->err = std::string("ncclAllReduce (capture): ") + ncclGetErrorString(r);
       return bail(BV_ENCCL);
     }
+    TRYC(cudaGraphInstantiate(&h->exec[kind], h->graph[kind], 0));
   }
-  TRYC(cudaGraphInstantiate(&h->exec, h->graph, 0));
   *out = h;
   g_setup_err.clear();
 #undef TRY
@@ -504,7 +599,7 @@ static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
   if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
   BV_CUDA(h, cudaSetDevice(h->device));
   fill_theta(*h->h_theta, theta);
-  BV_CUDA(h, cudaGraphLaunch(h->exec, h->stream));
+  BV_CUDA(h, cudaGraphLaunch(h->exec[h->h_theta->kind], h->stream));
   BV_CUDA(h, cudaStreamSynchronize(h->stream));
   const unsigned long long* acc = h->h_acc;
   if (acc[6] != 0) {
@@ -570,6 +665,9 @@ bv_status bv_last_error(const bv_handle* h, int32_t* failed_position, const char
 }
 
 void* bv_stream(const bv_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+// Debug builds only (-DBV_PROFILE_PHASES, libbv_prof.so): per-phase cycle sums.
+int bv_debug_phase_cycles(unsigned long long* out8, int reset) { return bv::debug_phase_cycles(out8, reset); }
 
 bv_status bv_last_kernel_ms(const bv_handle* h, float* ms) {
   if (!h || !ms) return BV_EINVAL;
