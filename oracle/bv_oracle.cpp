@@ -112,22 +112,29 @@ inline double perturb_entry(double v, int32_t a, int32_t b, uint32_t seed) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   z ^= z >> 31;
-  const int r = (int)(z % 3u);
-  if (r == 0) return std::nextafter(v, -INFINITY);
-  if (r == 2) return std::nextafter(v, INFINITY);
+  // seed s ≥ 1: a move of −s..+s ulp, uniform (the magnitude models an FP64
+  // Eq. (7) evaluation — sqrt, division, exp, products — a few ulp off)
+  const int span = 2 * (int)(seed >= 1000 ? seed / 1000 : 1) + 1;
+  const int r = (int)(z % (uint64_t)span) - (span - 1) / 2;
+  for (int i = 0; i < r; ++i) v = std::nextafter(v, INFINITY);
+  for (int i = 0; i > r; --i) v = std::nextafter(v, -INFINITY);
   return v;
 }
 inline long double perturb_entry(long double v, int32_t, int32_t, uint32_t) { return v; }
 
 /* Textbook unblocked Cholesky (Cholesky–Crout, column by column), row-major
  * lower factor in L (n×n, only j ≤ i used).  Returns false on a pivot that is
- * ≤ 0 or not finite (reading: non-PD → failure). */
-template <class R> bool potrf(const std::vector<R>& A, std::vector<R>& L, int n) {
+ * not > floor or not finite (reading G15: non-PD → failure; a covariance's
+ * pivots are compared with kPivotFloor·σ², σ² being every diagonal entry of
+ * Σθ, so an FP64-singular matrix — e.g. a repeated location, whose pivot is
+ * rounding noise of either sign — fails whatever the rounding order). */
+constexpr double kPivotFloor = 1e-14;
+template <class R> bool potrf(const std::vector<R>& A, std::vector<R>& L, int n, R floor = R(0)) {
   L.assign((size_t)n * n, R(0));
   for (int j = 0; j < n; ++j) {
     R s = A[(size_t)j * n + j];
     for (int k = 0; k < j; ++k) s -= L[(size_t)j * n + k] * L[(size_t)j * n + k];
-    if (!(s > R(0)) || !std::isfinite((double)s)) return false;
+    if (!(s > floor) || !std::isfinite((double)s)) return false;
     R ljj = std::sqrt(s);
     L[(size_t)j * n + j] = ljj;
     for (int i = j + 1; i < n; ++i) {
@@ -207,7 +214,7 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
         Scross[(size_t)a * l + c] = perturb_entry(matern<R>(dist<R>(loc(NN[a]), loc(B[c]), d), sigma2, beta, nu), NN[a], B[c], seed);
     // l.17  L ← POTRF(Σcon)
     std::vector<R> L;
-    if (!potrf<R>(Scon, L, m)) return 3;
+    if (!potrf<R>(Scon, L, m, R(kPivotFloor) * sigma2)) return 3;
     // l.18  Σ'cross ← TRSM(L, Σcross): column by column forward substitution
     std::vector<R> W = Scross;
     for (int c = 0; c < l; ++c) trsv<R>(L, m, W.data() + c, (size_t)l);
@@ -235,7 +242,7 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
   }
   // l.24  L' ← POTRF(Σnew)
   std::vector<R> Lp;
-  if (!potrf<R>(Snew, Lp, l)) return 3;
+  if (!potrf<R>(Snew, Lp, l, R(kPivotFloor) * sigma2)) return 3;
   // l.25  v ← TRSV(L', y_B − μnew)
   std::vector<R> v(l);
   for (int a = 0; a < l; ++a) v[a] = yB[a] - munew[a];
@@ -391,7 +398,7 @@ int or_exact_loglik(int64_t n, int d, const double* locs, const double* y, const
     for (int64_t i = 0; i < n; ++i)
       for (int64_t j = 0; j < n; ++j)
         S[(size_t)i * n + j] = matern<R>(dist<R>(locs + i * d, locs + j * d, d), s2, be, nu);
-    if (!potrf<R>(S, L, (int)n)) return 3;
+    if (!potrf<R>(S, L, (int)n, R(kPivotFloor) * s2)) return 3;
     std::vector<R> z(n);
     for (int64_t i = 0; i < n; ++i) z[i] = R(y[i]);
     trsv<R>(L, (int)n, z.data(), 1);
@@ -492,7 +499,7 @@ int or_simulate_bv(int64_t n, int d, const double* locs, int32_t bc, const int32
       for (int a = 0; a < N; ++a)
         for (int c = 0; c < N; ++c)
           S[(size_t)a * N + c] = matern<double>(dist<double>(locs + (size_t)J[a] * d, locs + (size_t)J[c] * d, d), s2, be, nu);
-      if (!potrf<double>(S, L, N)) {
+      if (!potrf<double>(S, L, N, kPivotFloor * s2)) {
 #ifdef _OPENMP
 #pragma omp critical
 #endif
@@ -524,7 +531,7 @@ int or_simulate_exact(int64_t n, int d, const double* locs, const double* theta,
   for (int64_t i = 0; i < n; ++i)
     for (int64_t j = 0; j < n; ++j)
       S[(size_t)i * n + j] = matern<double>(dist<double>(locs + i * d, locs + j * d, d), theta[0], theta[1], theta[2]);
-  if (!potrf<double>(S, L, (int)n)) return 3;
+  if (!potrf<double>(S, L, (int)n, kPivotFloor * theta[0])) return 3;
   for (int64_t i = 0; i < n; ++i) {
     double s = 0;
     for (int64_t j = 0; j <= i; ++j) s += L[(size_t)i * n + j] * eps[j];

@@ -35,14 +35,18 @@ def _stale():
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False, profile_phases: bool = False) -> str:
-    """Build libbv.so (or, with profile_phases, the debug-instrumented libbv_prof.so)."""
+def build(force: bool = False, verbose: bool = False, profile_phases: bool = False, variant: str = "",
+          defines=()) -> str:
+    """Build libbv.so (or, with profile_phases, the debug-instrumented libbv_prof.so;
+    with variant="x" and defines, an experimental libbv_x.so for A/B timing)."""
     out = LIB if not profile_phases else os.path.join(HERE, "libbv_prof.so")
-    if not profile_phases and not force and not _stale():
+    if variant:
+        out = os.path.join(HERE, f"libbv_{variant}.so")
+    if not profile_phases and not variant and not force and not _stale():
         return LIB
     inc, libdir = nccl_dirs()
     tmp = out + f".tmp{os.getpid()}"
-    extra = ["-DBV_PROFILE_PHASES"] if profile_phases else []
+    extra = (["-DBV_PROFILE_PHASES"] if profile_phases else []) + [f"-D{d}" for d in defines]
     cmd = (["nvcc", *ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
             "-Xptxas", "-v" if verbose else "-O3",
             "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc, "-o", tmp]
@@ -54,5 +58,7 @@ def build(force: bool = False, verbose: bool = False, profile_phases: bool = Fal
 
 
 if __name__ == "__main__":
+    var = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")]
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
-                profile_phases="--profile-phases" in sys.argv))
+                profile_phases="--profile-phases" in sys.argv, variant=var[0] if var else "", defines=defs))

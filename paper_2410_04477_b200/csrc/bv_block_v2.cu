@@ -15,17 +15,22 @@
 // Design:
 //  * tiles of 8×8; panel J = columns 8J..8J+7; rows up to N (the y row);
 //  * left-looking: panel J's tiles C(I,J) = A(I,J) − Σ_{K<J} L(I,K) L(J,K)ᵀ, the
-//    sum accumulated in registers by DMMA.8x8x4 (two accumulator chains), A
-//    generated on the fly from the gathered points (Matérn, Eq. 7) — the
-//    covariance never touches HBM;
-//  * diagonal tile factored in-lane by warp 0 (8 pivots, rsqrt), rows below
-//    solved one row per thread (forward substitution, not an explicit inverse);
-//  * only the live part of L is kept in shared memory: L(I,K) is needed from
-//    panel K+1 to panel I, so at panel J the live set is {K < J ≤ I}, at most
-//    T²/4 tiles; slots are recycled through a per-(TI,TJ) table computed once
-//    on the host (bv_host.cpp: build_slot_tables);
-//  * L tiles are stored in DMMA fragment order: element (g, k) at
-//    2·(4g + (k&3)) + (k>>2), so one LDS.128 per lane yields both k-halves.
+//    sum accumulated in registers by DMMA.8x8x4, A generated on the fly from
+//    the gathered points (Matérn, Eq. 7) — the covariance never touches HBM;
+//  * one warp per CTA factors the diagonal tiles (the block's serial pivot
+//    chain); it is the warp that runs on SM sub-partition 0 (%warpid mod 4),
+//    so the chains of all co-resident CTAs share one sub-partition while the
+//    three update warps of every CTA fill the other three FP64 pipes with the
+//    bulk (generation and DMMA) — no DMMA burst ever queues ahead of a pivot;
+//  * rows below the diagonal are solved one row per thread (forward
+//    substitution, not an explicit inverse), in place;
+//  * each tile lives in one shared-memory slot from generation (C, row-major)
+//    through the in-place solve (L, DMMA fragment order) to its last use;
+//    slots are recycled by a per-(TI,TJ) table built once on the host
+//    (bv_host.cpp: SlotTables) — at most ≈ T²/4 tiles are live;
+//  * L tiles in fragment order: element (g, k) at 2·(4g + (k&3)) + (k>>2), so
+//    one LDS.128 per lane yields both k-halves; a row keeps the same 64 bytes
+//    in both layouts, which is what makes the solve in place.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,8 +41,12 @@ namespace bv {
 
 namespace {
 
-constexpr int kW = 4;            // warps per CTA
-constexpr int kNT = kW * 32;     // threads per CTA
+constexpr int kW = 4;         // warps per CTA: 1 diagonal warp + 3 update warps
+constexpr int kNT = kW * 32;  // threads per CTA
+#ifndef BV_GEN_UNROLL
+#define BV_GEN_UNROLL 4
+#endif
+constexpr int kGenUnroll = BV_GEN_UNROLL;  // Matérn entries in flight per thread
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -58,27 +67,28 @@ __device__ __forceinline__ void sts2(double* p, double a, double b) {
 // after B, 6 phase C + sync, 7 CTAs, 8 GEMM part of 2, 9 generation part of 2.
 __device__ unsigned long long g_phase_cycles[10];
 #define PH_T(v) long long v = clock64()
-#define PH_ADD(i, v0) do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(clock64() - (v0))); } while (0)
+#define PH_ADD(i, v0)                                                                                   \
+  do {                                                                                                  \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(clock64() - (v0))); \
+  } while (0)
 #else
 #define PH_T(v)
 #define PH_ADD(i, v0)
 #endif
 
 // Shared-memory carve-up (in doubles) for a bucket with at most TImax tile rows
-// and `cap` L slots.
+// and `cap` tile slots.
 struct V2Layout {
-  int P, stage, stage2, diag, rinv, misc, theta, etab, slots, tab, total_bytes;
+  int P, diag, rinv, misc, theta, etab, slots, tab, total_bytes;
   __host__ __device__ V2Layout(int TImax, int cap) {
-    P = 0;                          // PointRec[8·TImax]
-    stage = P + 32 * TImax;         // TImax tiles, row-major 8×8 (panel J)
-    stage2 = stage + 64 * TImax;    // the same for panel J+1 (double buffer)
-    diag = stage2 + 64 * TImax;     // factored diagonal tile (row-major lower)
-    rinv = diag + 64;               // 1/L_jj of the diagonal tile
-    misc = rinv + 8;                // [0] logdet, [1] quad, [2] fail
-    theta = misc + 8;               // Theta copy (16 doubles + ints → 20 doubles)
-    etab = theta + 20;              // 2^{−j/64}, j = 0..63 (exp_neg table)
-    slots = etab + 64;              // cap L tiles in fragment order
-    tab = slots + 64 * cap;         // int16 slot table (TImax²), in doubles:
+    P = 0;                   // PointRec[8·TImax]
+    diag = P + 32 * TImax;   // factored diagonal tile (row-major lower; diagonal = L_jj)
+    rinv = diag + 64;        // 1/L_jj of the diagonal tile
+    misc = rinv + 8;         // [0] logdet, [1] quad, [2] fail, [3] diagonal warp
+    theta = misc + 8;        // Theta copy (16 doubles + ints → 20 doubles)
+    etab = theta + 20;       // 2^{−j/64}, j = 0..63 (exp_neg table)
+    slots = etab + 64;       // cap tiles
+    tab = slots + 64 * cap;  // int16 slot table (TImax²), in doubles:
     total_bytes = (tab + (TImax * TImax + 3) / 4) * 8;
   }
 };
@@ -96,75 +106,120 @@ __device__ __forceinline__ double joint_entry(const PointRec* P, int r, int c, i
   return (c >= N || r > N) ? 0.0 : v;
 }
 
-// One warp, in-lane: Cholesky of the diagonal tile held row-major in `stage`
-// (lower part).  Publishes L's strict lower part (incl. the y row when it sits
-// inside this tile) and 1/L_jj (0 on padding columns), adds the panel's
-// Σ_{j≥m} log p_j to d, and raises the non-PD flag.
-__device__ __forceinline__ void factor_diag_tile(const double* stage, double* diagL, double* rinv, double* misc,
-                                                 int J, int m, int N, int lane) {
+// One warp, in-lane (every lane holds the whole tile; no shuffles or memory
+// in the pivot chain, ~55 cycles per pivot): Cholesky of the diagonal tile
+// held row-major (lower part) in its slot.  Publishes L's strict lower part
+// and 1/L_jj (0 on padding columns); accumulates, in the caller's registers,
+// the product of the block pivots j ≥ m (for d, one log per block), the y
+// row's Σ_{j≥m} L_Nj² when the y row sits inside this tile (for u), and the
+// count of bad pivots (non-PD).
+__device__ __forceinline__ void factor_diag_tile(const double* tile, double* diagL, double* rinv, int J, int m, int N,
+                                                 int lane, double pfloor, double& prod, int& nbad, double& qd) {
+  const int nreal = N - 8 * J;  // columns j < nreal are real pivots
+  const int jm = m - 8 * J;     // columns j ≥ jm belong to the block (contribute to d)
+  const int yr = N - 8 * J;     // the y row inside this tile (N not a multiple of 8)
   double a[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j <= i; ++j) a[i][j] = stage[8 * i + j];
-  double rv[8];
-  double prod = 1.0;  // Π_{j≥m} p_j over this panel (≤ 8 pivots: no over/underflow for sane θ)
-  int nbad = 0;
-  const int nreal = N - 8 * J;   // columns j < nreal are real pivots
-  const int jm = m - 8 * J;      // columns j ≥ jm belong to the block (contribute to d)
+    for (int k = 0; k <= i; ++k) a[i][k] = tile[8 * i + k];
+  double rv[8], lv[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     double p = a[j][j];
-    const bool ok = (p > 0.0) & (p <= 1.7976931348623157e308);
+    // non-PD (reading G15): a pivot not above kPivotFloor·σ² — FP64-singular
+    const bool ok = (p > pfloor) & (p <= 1.7976931348623157e308);
     const bool real = j < nreal;
     nbad += (real & !ok) ? 1 : 0;
     p = (real & ok) ? p : 1.0;
     prod *= (j >= jm) ? p : 1.0;
-    rv[j] = real ? rsqrt_pos(p) : 0.0;
+    const double r = rsqrt_pos(p);
+    rv[j] = real ? r : 0.0;
+    lv[j] = p * r;  // L_jj = √p (≤ 1 ulp)
+    // L_ij = a_ij / L_jj: scale by r, then one residual correction so each
+    // entry is rounded on its own (a systematic per-column scale error would be
+    // amplified by the ill-conditioned Schur complements of late blocks)
 #pragma unroll
-    for (int i = j + 1; i < 8; ++i) a[i][j] *= rv[j];
+    for (int i = j + 1; i < 8; ++i) {
+      const double x = a[i][j] * rv[j];
+      a[i][j] = fma(fma(-x, lv[j], a[i][j]), rv[j], x);
+    }
 #pragma unroll
     for (int i = j + 1; i < 8; ++i)
 #pragma unroll
       for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-    if (lane == i) {
+  for (int i = 1; i < 8; ++i)
+    if (i == yr) {
 #pragma unroll
-      for (int j = 0; j < i; ++j) diagL[8 * i + j] = a[i][j];
-      rinv[i] = rv[i];
+      for (int k = 0; k < i; ++k)
+        if (k >= jm) qd = fma(a[i][k], a[i][k], qd);
     }
   if (lane == 0) {
-    misc[0] += log(prod);  // d = Σ_{j≥m} log p_j (a8)
-    if (nbad) misc[2] = 1.0;
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < i; ++k) diagL[8 * i + k] = a[i][k];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      rinv[k] = rv[k];
+      diagL[9 * k] = lv[k];  // the diagonal slots hold L_jj
+    }
   }
 }
 
-// a3: generate the row-major tiles I = I0 .. I0+ntiles−1 of column panel J
-// into dst (tile i at dst + 64·i), entries spread over `nthr` threads.  A
-// plain loop (two entries in flight per thread): one copy of the Matérn code
-// keeps the kernel inside the instruction cache.
-template <int KIND>
-__device__ __forceinline__ void gen_tiles(const PointRec* P, int N, const Theta& th, const double* tab64, double* dst,
-                                          int I0, int ntiles, int J, int thr, int nthr) {
-  const int total = ntiles * 64;
+// Panel update on the tensor cores for the NS tiles I = J+1+(u−1)+3s of update
+// warp u: S(s) += Σ_{K<J} L(I,K) L(J+1,K)ᵀ, two DMMA.8x8x4 per (tile, K).
+template <int NS, int MAXT>
+__device__ __forceinline__ void panel_gemm(double (&S0)[MAXT][2], const double* slots, const int16_t* tab, int TI,
+                                           int J, int uw, int lane) {
+  const int16_t* tJ = tab + (J + 1) * TI;
+  const int16_t* tI[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) tI[s] = tab + (J + uw + (kW - 1) * s) * TI;
 #pragma unroll 2
-  for (int e = thr; e < total; e += nthr) {
-    const int r = 8 * I0 + (e >> 3);  // (tile, row) flattened: 8·(I0 + e/64) + (e/8)%8
-    const int c = 8 * J + (e & 7);
-    dst[e] = joint_entry<KIND>(P, r, c, N, th, tab64);
+  for (int K = 0; K < J; ++K) {
+    const double2 b = lds2(slots + 64 * tJ[K] + 2 * lane);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const double2 a = lds2(slots + 64 * tI[s][K] + 2 * lane);
+      dmma884(S0[s][0], S0[s][1], a.x, b.x);
+      dmma884(S0[s][0], S0[s][1], a.y, b.y);
+    }
   }
 }
+
+// a3: generate the row-major tiles I = I0 .. TI−1 of column panel J into their
+// slots, entries spread over `nthr` threads.  A plain loop (BV_GEN_UNROLL
+// entries in flight per thread): few copies of the Matérn code keep the kernel
+// inside the instruction cache.
+template <int KIND>
+__device__ __forceinline__ void gen_tiles(const PointRec* P, int N, const Theta& th, const double* tab64,
+                                          double* slots, const int16_t* tab, int TI, int I0, int J, int thr,
+                                          int nthr) {
+  const int total = (TI - I0) * 64;
+#pragma unroll(kGenUnroll)
+  for (int e = thr; e < total; e += nthr) {
+    const int I = I0 + (e >> 6);
+    const int r = 8 * I + ((e >> 3) & 7);
+    const int c = 8 * J + (e & 7);
+    slots[64 * tab[I * TI + J] + (e & 63)] = joint_entry<KIND>(P, r, c, N, th, tab64);
+  }
+}
+
+#ifndef BV_MINB
+#define BV_MINB 4  // CTAs per SM the register allocation targets (4 × 128 threads → ≤ 128 registers)
+#endif
 
 template <int MAXT, int KIND>
-__global__ void __launch_bounds__(kNT, 4)
+__global__ void __launch_bounds__(kNT, BV_MINB)
 bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__ nbr,
                    const BlockDesc* __restrict__ desc, const int32_t* __restrict__ list,
                    const Theta* __restrict__ theta_dev, const int16_t* __restrict__ tabs,
                    const int32_t* __restrict__ tab_off, const double* __restrict__ exp_tab, int TImax, int cap,
-                   double* __restrict__ out_u, double* __restrict__ out_d, uint32_t* __restrict__ limbs,
-                   int32_t* __restrict__ status) {
+                   double* __restrict__ out_u, double* __restrict__ out_d, unsigned long long* __restrict__ acc,
+                   int k_begin) {
   extern __shared__ __align__(16) double smem[];
   const V2Layout Ly(TImax, cap);
   const int q = list[blockIdx.x];
@@ -174,15 +229,8 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   const int TI = (N + 8) >> 3;  // tile rows (rows 0..N, incl. the y row)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  // Role rotation across co-resident CTAs: the diagonal warp is blockIdx mod 4,
-  // the update warps are numbered u = 1..3 after it.
-  const int dwarp = blockIdx.x & 3;
-  const int uw = (warp - dwarp) & 3;  // 0 = diagonal warp, 1..3 = update warps
-  const int utid = (uw - 1) * 32 + lane;  // 0..95 among the update warps
 
   PointRec* P = reinterpret_cast<PointRec*>(smem + Ly.P);
-  double* stage = smem + Ly.stage;
-  double* stage2 = smem + Ly.stage2;
   double* diagL = smem + Ly.diag;
   double* rinv = smem + Ly.rinv;
   double* misc = smem + Ly.misc;
@@ -206,23 +254,39 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
 #pragma unroll 1
     for (int e = tid; e < TI * TI; e += kNT) tab[e] = gt[e];
   }
-  if (tid < 8) misc[tid] = 0.0;
+  if (tid < 4) misc[tid] = 0.0;
   __syncthreads();
+  // The diagonal warp is the one on sub-partition 0 (a CTA's four warps sit on
+  // the four sub-partitions); warp 0 if none reports it.
+  {
+    unsigned wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    if (lane == 0 && (wid & 3u) == 0u) misc[3] = (double)warp;
+  }
+  __syncthreads();
+  const int dwarp = (int)misc[3];
+  const int uw = (warp - dwarp) & (kW - 1);  // 0 = diagonal warp, 1..3 = update warps
+  const int utid = (uw - 1) * 32 + lane;     // 0..95 among the update warps
   const Theta& th = *ths;
+  // diagonal-warp accumulators (registers, whole block): Π pivots as pm·2^pe,
+  // y-row quadratic form inside diagonal tiles, bad-pivot count
+  double pm = 1.0, qd = 0.0;
+  int pe = 0, nbad = 0;
   PH_T(t_pro);
 
   // panel 0: C(I,0) = A(I,0) (nothing to subtract yet), all warps
-  gen_tiles<KIND>(P, N, th, etab, stage, 0, TI, 0, tid, kNT);
+  gen_tiles<KIND>(P, N, th, etab, slots, tab, TI, 0, 0, tid, kNT);
   __syncthreads();
   PH_ADD(0, t_pro);
 
-  // Pipeline per panel J (stage holds the final C(I,J), I ≥ J, tile I at
-  // stage + 64·(I−J), on entry):
+  // Pipeline per panel J (the slots of column J hold the final C(I,J), I ≥ J,
+  // row-major, on entry — each tile is staged in the slot its L will occupy):
   //   A: the diagonal warp factors tile (J,J) while the update warps u = 1..3
-  //      generate A(·,J+1) into stage2 and accumulate, in registers on the
-  //      tensor cores, S(I) = Σ_{K<J} L(I,K) L(J+1,K)ᵀ for I = J+1+(u−1)+3s;
-  //   B: all warps: L(I,J) = C(I,J) L(J,J)⁻ᵀ for I > J, one row per thread;
-  //   C: update warps: C(I,J+1) = A − S(I) − L(I,J) L(J+1,J)ᵀ in stage2; swap.
+  //      generate A(·,J+1) into column J+1's slots and accumulate, in registers
+  //      on the tensor cores, S(I) = Σ_{K<J} L(I,K) L(J+1,K)ᵀ, I = J+1+(u−1)+3s;
+  //   B: all warps: L(I,J) = C(I,J) L(J,J)⁻ᵀ for I > J, one row per thread, in
+  //      place (a row occupies the same 64 bytes in both layouts);
+  //   C: update warps: C(I,J+1) = A − S(I) − L(I,J) L(J+1,J)ᵀ in place.
   for (int J = 0; J < TJ; ++J) {
     const bool ahead = (J + 1 < TJ);
     double S0[MAXT][2];  // one DMMA chain per tile; tiles interleave for ILP
@@ -230,26 +294,29 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     for (int s = 0; s < MAXT; ++s) S0[s][0] = S0[s][1] = 0.0;
     PH_T(t_a);
     if (uw == 0) {
-      factor_diag_tile(stage, diagL, rinv, misc, J, m, N, lane);
+      factor_diag_tile(slots + 64 * tab[J * TI + J], diagL, rinv, J, m, N, lane, kPivotFloor * th.sigma2, pm, nbad,
+                       qd);
+      int ex;
+      pm = frexp(pm, &ex);  // keep the running product of ≤ N pivots in range
+      pe += ex;
+      if (nbad && lane == 0) misc[2] = 1.0;
       PH_ADD(1, t_a);
     } else if (ahead) {
       PH_T(t_gen);
-      gen_tiles<KIND>(P, N, th, etab, stage2, J + 1, TI - J - 1, J + 1, utid, 96);
+      gen_tiles<KIND>(P, N, th, etab, slots, tab, TI, J + 1, J + 1, utid, (kW - 1) * 32);
       PH_ADD(9, t_gen);
       PH_T(t_gm);
-      const int16_t* tJ = tab + (J + 1) * TI;
-#pragma unroll 2
-      for (int K = 0; K < J; ++K) {
-        const double2 b = lds2(slots + 64 * tJ[K] + 2 * lane);
-#pragma unroll
-        for (int s = 0; s < MAXT; ++s) {
-          const int I = J + uw + (kW - 1) * s;
-          if (I < TI) {
-            const double2 a = lds2(slots + 64 * tab[I * TI + K] + 2 * lane);
-            dmma884(S0[s][0], S0[s][1], a.x, b.x);
-            dmma884(S0[s][0], S0[s][1], a.y, b.y);
-          }
-        }
+      // exactly ns = ⌈(TI−J−1−(u−1))/3⌉ tiles: no predicated-off DMMA issue
+      const int ns = (TI - J - 1 - (uw - 1) + (kW - 2)) / (kW - 1);
+      switch (ns) {
+#define BV_NS(n)                                                                          \
+  case n:                                                                                 \
+    if (MAXT >= n) panel_gemm<(MAXT >= n ? n : 1), MAXT>(S0, slots, tab, TI, J, uw, lane); \
+    break;
+        BV_NS(1) BV_NS(2) BV_NS(3) BV_NS(4) BV_NS(5) BV_NS(6) BV_NS(7) BV_NS(8) BV_NS(9) BV_NS(10) BV_NS(11)
+        BV_NS(12)
+#undef BV_NS
+        default: break;
       }
 #ifdef BV_PROFILE_PHASES
       if (S0[0][0] == 12345.678) misc[7] = S0[0][1];
@@ -263,22 +330,12 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     if (misc[2] != 0.0) break;
     PH_T(t_b);
 
-    // B: rows below the diagonal tile (a5/a6), stored in fragment order
-    if (tid == 0) {  // the y row inside the diagonal tile (N not a multiple of 8)
-      const int yr = N - 8 * J;
-      if (yr > 0 && yr < 8) {
-        double qd = 0.0;
-#pragma unroll 1
-        for (int j = 0; j < yr; ++j)
-          if (8 * J + j >= m) qd = fma(diagL[8 * yr + j], diagL[8 * yr + j], qd);
-        misc[1] += qd;
-      }
-    }
+    // B: rows below the diagonal tile (a5/a6), solved in place into fragment order
     const int rows = (TI - J - 1) * 8;
     for (int rr = tid; rr < rows; rr += kNT) {
       const int I = J + 1 + (rr >> 3);
       const int gg = rr & 7;
-      const double* src = stage + 64 * (I - J) + 8 * gg;
+      double* src = slots + 64 * tab[I * TI + J] + 8 * gg;  // C(I,J) row gg → L(I,J) row gg
       double c[8], x[8];
 #pragma unroll
       for (int k = 0; k < 8; k += 2) {
@@ -291,7 +348,10 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         double tv = c[k];
 #pragma unroll
         for (int kk = 0; kk < k; ++kk) tv = fma(-x[kk], diagL[8 * k + kk], tv);
-        x[k] = tv * rinv[k];  // rinv = 0 on padding columns → x = 0
+        // tv / L_kk: scaled by 1/L_kk, then one residual correction (rinv = 0 on
+        // padding columns → x = 0)
+        const double xk = tv * rinv[k];
+        x[k] = fma(fma(-xk, diagL[9 * k], tv), rinv[k], xk);
       }
       if (8 * I + gg == N) {  // the y row: u = Σ_{j≥m} z_j² (a8)
         double qd = 0.0;
@@ -300,9 +360,8 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           if (8 * J + k >= m && 8 * J + k < N) qd = fma(x[k], x[k], qd);
         misc[1] += qd;
       }
-      double* dst = slots + 64 * tab[I * TI + J] + 8 * gg;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) sts2(dst + 2 * k, x[k], x[k + 4]);
+      for (int k = 0; k < 4; ++k) sts2(src + 2 * k, x[k], x[k + 4]);
     }
     PH_ADD(4, t_b);
     PH_T(t_s2);
@@ -311,7 +370,7 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     if (!ahead) break;
     PH_T(t_c);
 
-    // C: last term of panel J+1's update, then publish C(I,J+1)
+    // C: last term of panel J+1's update, then publish C(I,J+1) in place
     if (uw > 0) {
       const double2 b = lds2(slots + 64 * tab[(J + 1) * TI + J] + 2 * lane);
 #pragma unroll
@@ -321,15 +380,12 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           const double2 a = lds2(slots + 64 * tab[I * TI + J] + 2 * lane);
           dmma884(S0[s][0], S0[s][1], a.x, b.x);
           dmma884(S0[s][0], S0[s][1], a.y, b.y);
-          double* cp = stage2 + 64 * (I - J - 1) + 8 * g + 2 * t;
+          double* cp = slots + 64 * tab[I * TI + J + 1] + 8 * g + 2 * t;
           const double2 av = lds2(cp);
           sts2(cp, av.x - S0[s][0], av.y - S0[s][1]);
         }
       }
     }
-    double* tmp = stage;
-    stage = stage2;
-    stage2 = tmp;
     __syncthreads();
     PH_ADD(6, t_c);
   }
@@ -337,22 +393,22 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   if (threadIdx.x == 0) atomicAdd(&g_phase_cycles[7], 1ull);
 #endif
 
-  // ---- a8: per-block outputs and the exact fixed-point term
-  if (tid == 0) {
+  // ---- a8: per-block outputs and the exact fixed-point term (the diagonal
+  // warp holds d's pivot product; u's TRSM part is in misc[1], visible since
+  // the loop's last barrier)
+  if (uw == 0 && lane == 0) {
     const bool fail = misc[2] != 0.0;
     int st = fail ? kNotPD : kOk;
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
-    const double logdet = fail ? 0.0 : misc[0];
-    const double quad = fail ? 0.0 : misc[1];
+    const double logdet = fail ? 0.0 : log(pm) + (double)pe * 0.69314718055994530942;  // d = Σ_{j≥m} log p_j
+    const double quad = fail ? 0.0 : misc[1] + qd;
     if (!fail) {
       const double tk = -0.5 * (quad + logdet + (double)l * kLn2Pi);
       if (fixed_encode(tk, c)) st = kTermRange;
     }
     out_u[q] = quad;
     out_d[q] = logdet;
-#pragma unroll
-    for (int i = 0; i < 6; ++i) limbs[(size_t)q * 6 + i] = c[i];
-    status[q] = st;
+    accumulate_term(acc, c, st, k_begin + q);  // a9
   }
 }
 
@@ -373,8 +429,8 @@ int debug_phase_cycles(unsigned long long* out, int reset) {
 }
 
 int v2_maxt_for(int TI) {
-  const int need = (TI - 1 + (kW - 2)) / (kW - 1);  // panel J+1 tiles over warps 1..3
-  const int opts[] = {2, 4, 5, 6, 8, 10, 12};
+  const int need = (TI - 1 + (kW - 2)) / (kW - 1);  // panel J+1 tiles over the update warps
+  const int opts[] = {1, 2, 3, 4, 5, 6, 8, 10, 12};
   for (int o : opts)
     if (o >= need) return o;
   return -1;
@@ -398,7 +454,9 @@ static cudaError_t prep_kinds(size_t smem) {
 
 cudaError_t prepare_block_v2(size_t max_smem) {
   cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = prep_kinds<1>(max_smem);
   if (e == cudaSuccess) e = prep_kinds<2>(max_smem);
+  if (e == cudaSuccess) e = prep_kinds<3>(max_smem);
   if (e == cudaSuccess) e = prep_kinds<4>(max_smem);
   if (e == cudaSuccess) e = prep_kinds<5>(max_smem);
   if (e == cudaSuccess) e = prep_kinds<6>(max_smem);
@@ -412,10 +470,10 @@ template <int MAXT>
 static void launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                         const BlockDesc* desc, const int32_t* list, const Theta* th, const int16_t* tabs,
                         const int32_t* tab_off, const double* etab, int TImax, int cap, double* u, double* d,
-                        uint32_t* limbs, int32_t* status) {
-#define BV_K(KD)                                                                                             \
+                        unsigned long long* acc, int k_begin) {
+#define BV_K(KD)                                                                                              \
   bv_block_v2_kernel<MAXT, KD><<<nblocks, kNT, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, \
-                                                          cap, u, d, limbs, status)
+                                                          cap, u, d, acc, k_begin)
   switch (kind) {
     case 0: BV_K(0); break;
     case 1: BV_K(1); break;
@@ -428,17 +486,17 @@ static void launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, cons
 cudaError_t launch_block_v2(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            uint32_t* limbs, int32_t* status) {
+                            unsigned long long* acc, int k_begin) {
   if (nblocks == 0) return cudaSuccess;
   const size_t smem = v2_smem_bytes(TImax, cap);
   switch (v2_maxt_for(TImax)) {
-    case 2: launch_kind<2>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, limbs, status); break;
-    case 4: launch_kind<4>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, limbs, status); break;
-    case 5: launch_kind<5>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, limbs, status); break;
-    case 6: launch_kind<6>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, limbs, status); break;
-    case 8: launch_kind<8>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, limbs, status); break;
-    case 10: launch_kind<10>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, limbs, status); break;
-    case 12: launch_kind<12>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, limbs, status); break;
+#define BV_MT(MT)                                                                                                \
+  case MT:                                                                                                       \
+    launch_kind<MT>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, acc, \
+                    k_begin);                                                                                   \
+    break;
+    BV_MT(1) BV_MT(2) BV_MT(3) BV_MT(4) BV_MT(5) BV_MT(6) BV_MT(8) BV_MT(10) BV_MT(12)
+#undef BV_MT
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

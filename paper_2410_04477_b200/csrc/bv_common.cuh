@@ -41,6 +41,11 @@ struct alignas(32) PointRec {
 // (Alg. 1 l.29).
 constexpr double kLn2Pi = 0x1.d67f1c864beb5p+0;
 
+// Non-PD rule (reading G15): a Cholesky pivot must exceed
+// kPivotFloor·σ² (σ² = every diagonal entry of Σθ); below it the block is
+// FP64-singular (e.g. a repeated location) whatever the rounding order.
+constexpr double kPivotFloor = 1e-14;
+
 // Block status codes written by the kernels.
 enum BlockStatus : int32_t { kOk = 0, kNotPD = 1, kTermRange = 2 };
 
@@ -99,7 +104,23 @@ __host__ __device__ inline int fixed_encode(double t, uint32_t c[6]) {
 }
 
 // Reduction result slots (uint64): [0..5] chunk sums, [6] failed-block count,
-// [7] local smallest failing position (UINT64_MAX if none).
+// [7] local smallest failing (position << 8 | status), UINT64_MAX if none.
 constexpr int kAccSlots = 8;
+
+#ifdef __CUDACC__
+// a9: add one block's exact term to the evaluation's accumulator.  Integer
+// atomics are associative, so the sum is independent of the order blocks
+// finish in (and of bucket schedule and GPU count).  Each slot receives < 2³²
+// additions of < 2³² → no uint64 overflow.
+__device__ __forceinline__ void accumulate_term(unsigned long long* acc, const uint32_t c[6], int st, int k) {
+#pragma unroll
+  for (int i = 0; i < 6; ++i)
+    if (c[i]) atomicAdd(acc + i, (unsigned long long)c[i]);
+  if (st != kOk) {
+    atomicAdd(acc + 6, 1ull);
+    atomicMin(acc + 7, ((unsigned long long)k << 8) | (unsigned long long)st);
+  }
+}
+#endif
 
 }  // namespace bv

@@ -4,9 +4,10 @@
 // lays it out on the device (block-contiguous 32-byte point records, neighbour
 // lists remapped to permuted indices), splits positions across ranks by
 // estimated cost, groups this rank's blocks into size buckets, creates the
-// NCCL communicator and captures ONE CUDA graph per handle:
-//   memcpy θ → bucket kernels (Alg. 1 l.10-29 fused per block) → exact
-//   reduction (l.28-30) → [ncclAllReduce of 7 uint64] → memcpy result.
+// NCCL communicator and captures one CUDA graph per Matérn kind:
+//   memcpy θ → zero accumulator → bucket kernels on concurrent branches
+//   (Alg. 1 l.10-29 fused per block, each block adding its exact fixed-point
+//   term atomically: l.28-30) → [ncclAllReduce of 7 uint64] → memcpy result.
 // bv_loglik: fills θ (and ν-only constants) into pinned memory, replays the
 // graph, decodes the exact fixed-point sum.
 #include <cuda_runtime.h>
@@ -28,9 +29,7 @@ size_t v1_smem_bytes(int Nmax);
 cudaError_t prepare_block_v1(int Nmax);
 cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                             const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
-                            uint32_t* limbs, int32_t* status);
-cudaError_t launch_reduce(const uint32_t* limbs, const int32_t* status, int nq, int k_begin,
-                          unsigned long long* acc, cudaStream_t s);
+                            unsigned long long* acc, int k_begin);
 cudaError_t launch_scatter_y(const double* y, const int32_t* perm_of_id, int64_t n, PointRec* pts, cudaStream_t s);
 int v2_maxt_for(int TI);
 int debug_phase_cycles(unsigned long long* out, int reset);
@@ -39,7 +38,7 @@ cudaError_t prepare_block_v2(size_t max_smem);
 cudaError_t launch_block_v2(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            uint32_t* limbs, int32_t* status);
+                            unsigned long long* acc, int k_begin);
 }  // namespace bv
 
 namespace {
@@ -51,12 +50,16 @@ struct Bucket {
   int cap;                  // v2: L slots for this TI
 };
 
-// L-slot recycling tables for the v2 kernel (bv_block_v2.cu).  For a block
-// with TI tile rows and TJ column panels, tile L(I,K) lives from the end of
-// panel K to panel I; row J's tiles are dead once panel J's update has read
-// them, and panel J then writes column J.  Simulate that with a LIFO free
-// list; slot[I·TI + K] is the slot of L(I,K).  off[2·TI + (TI−TJ)] indexes
-// the table of each (TI, TJ) pair (TI − TJ ∈ {0, 1}); cap[TI] = max slots.
+// Slot tables for the v2 kernel (bv_block_v2.cu).  Every tile of column K
+// lives in one shared-memory slot from its generation (C, row-major) through
+// its in-place triangular solve (L, fragment order) until its last use.  For a
+// block with TI tile rows and TJ column panels: column 0 is generated first;
+// iteration J generates column J+1 (tiles I ≥ J+1) at its start, after
+// freeing row J's L tiles (last read in iteration J−1) and the diagonal tile
+// (J−1,J−1) (consumed by iteration J−1's factorisation).  A LIFO free list
+// replays that schedule; slot[I·TI + K] is the slot of tile (I,K).
+// off[2·TI + (TI−TJ)] indexes the table of each (TI, TJ) pair (TI − TJ ∈
+// {0, 1}); cap[TI] = the most slots live at once.
 struct SlotTables {
   std::vector<int16_t> tabs;
   std::vector<int32_t> off;
@@ -69,24 +72,32 @@ struct SlotTables {
       for (int e = 0; e < 2; ++e) {
         const int TJ = TI - e;
         off[2 * TI + e] = (int32_t)tabs.size();
-        std::vector<int16_t> t((size_t)TI * TI, -1);
+        std::vector<int16_t> t((size_t)TI * TI, 0);
         std::vector<int16_t> freel;
-        int next = 0;
-        for (int J = 0; J < TJ; ++J) {
-          for (int K = 0; K < J; ++K) freel.push_back(t[(size_t)J * TI + K]);
-          for (int I = J + 1; I < TI; ++I) {
-            if (!freel.empty()) {
-              t[(size_t)I * TI + J] = freel.back();
-              freel.pop_back();
-            } else {
-              t[(size_t)I * TI + J] = (int16_t)next++;
-            }
+        int next = 0, live = 0, most = 0;
+        auto alloc = [&]() -> int16_t {
+          ++live;
+          most = std::max(most, live);
+          if (!freel.empty()) {
+            int16_t v = freel.back();
+            freel.pop_back();
+            return v;
           }
+          return (int16_t)next++;
+        };
+        auto release = [&](int16_t v) {
+          --live;
+          freel.push_back(v);
+        };
+        for (int I = 0; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
+        for (int J = 0; J < TJ; ++J) {
+          if (J >= 1) release(t[(size_t)(J - 1) * TI + (J - 1)]);
+          for (int K = 0; K < J; ++K) release(t[(size_t)J * TI + K]);
+          if (J + 1 < TJ)
+            for (int I = J + 1; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
         }
-        for (auto& v : t)
-          if (v < 0) v = 0;
         tabs.insert(tabs.end(), t.begin(), t.end());
-        cap[TI] = std::max(cap[TI], std::max(next, 1));
+        cap[TI] = std::max(cap[TI], std::max(most, 1));
       }
   }
 };
@@ -108,8 +119,6 @@ struct bv_handle {
   bv::Theta* d_theta = nullptr;
   double* d_u = nullptr;
   double* d_d = nullptr;
-  uint32_t* d_limbs = nullptr;
-  int32_t* d_status = nullptr;
   unsigned long long* d_acc = nullptr;
   unsigned long long* d_min = nullptr;
   int32_t* d_perm_of_id = nullptr;
@@ -121,6 +130,9 @@ struct bv_handle {
   bv::Theta* h_theta = nullptr;            // pinned
   unsigned long long* h_acc = nullptr;     // pinned
   cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // around the block kernels (graph event nodes)
+  static constexpr int kBranches = 4;             // concurrent bucket streams inside the graph
+  cudaStream_t side[kBranches] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t fork_ev = nullptr, join_ev[kBranches] = {nullptr, nullptr, nullptr, nullptr};
   std::vector<Bucket> buckets;
   std::string err;
   int32_t failed_pos = -1;
@@ -214,12 +226,17 @@ void release(bv_handle* h) {
     h->graph[k] = nullptr;
   }
   if (h->comm) ncclCommDestroy(h->comm);
-  void* dev[] = {h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d, h->d_limbs,
-                 h->d_status, h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
+  void* dev[] = {h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d,
+                 h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (h->h_theta) cudaFreeHost(h->h_theta);
   if (h->h_acc) cudaFreeHost(h->h_acc);
+  for (int b = 0; b < bv_handle::kBranches; ++b) {
+    if (h->side[b]) cudaStreamDestroy(h->side[b]);
+    if (h->join_ev[b]) cudaEventDestroy(h->join_ev[b]);
+  }
+  if (h->fork_ev) cudaEventDestroy(h->fork_ev);
   if (h->ev_k0) cudaEventDestroy(h->ev_k0);
   if (h->ev_k1) cudaEventDestroy(h->ev_k1);
   if (h->stream) cudaStreamDestroy(h->stream);
@@ -521,8 +538,6 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   TRY(upload<bv::Theta>(h, &h->d_theta, nullptr, 1));
   TRY(upload<double>(h, &h->d_u, nullptr, (size_t)h->nq));
   TRY(upload<double>(h, &h->d_d, nullptr, (size_t)h->nq));
-  TRY(upload<uint32_t>(h, &h->d_limbs, nullptr, (size_t)h->nq * 6));
-  TRY(upload<int32_t>(h, &h->d_status, nullptr, (size_t)h->nq));
   TRY(upload<unsigned long long>(h, &h->d_acc, nullptr, bv::kAccSlots));
   TRY(upload<unsigned long long>(h, &h->d_min, nullptr, 1));
   TRYC(cudaMallocHost((void**)&h->h_theta, sizeof(bv::Theta)));
@@ -550,24 +565,42 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
 
   TRYC(cudaEventCreate(&h->ev_k0));
   TRYC(cudaEventCreate(&h->ev_k1));
-  // capture the per-evaluation graph, one per Matérn kind (the block kernel is
-  // specialised on it; the kind is chosen from ν at each evaluation)
+  TRYC(cudaEventCreateWithFlags(&h->fork_ev, cudaEventDisableTiming));
+  for (int b = 0; b < bv_handle::kBranches; ++b) {
+    TRYC(cudaStreamCreateWithFlags(&h->side[b], cudaStreamNonBlocking));
+    TRYC(cudaEventCreateWithFlags(&h->join_ev[b], cudaEventDisableTiming));
+  }
+  // Capture the per-evaluation graph, one per Matérn kind (the block kernel is
+  // specialised on it; the kind is chosen from ν at each evaluation):
+  //   θ upload → zero the accumulator → bucket kernels (largest first, spread
+  //   over kBranches concurrent graph branches so small buckets overlap big
+  //   ones instead of draining the GPU between launches; each block adds its
+  //   exact term atomically) → [ncclAllReduce] → result to the host.
   for (int kind = 0; kind < 4; ++kind) {
     TRYC(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
     cudaError_t e = cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta), cudaMemcpyHostToDevice, h->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->d_acc, 0, sizeof(unsigned long long) * 7, h->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->d_acc + 7, 0xff, sizeof(unsigned long long), h->stream);
     if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k0, h->stream, cudaEventRecordExternal);
-    for (const Bucket& b : h->buckets) {
-      if (e != cudaSuccess) break;
+    if (e == cudaSuccess) e = cudaEventRecord(h->fork_ev, h->stream);
+    const int nbr_streams = std::min<int>(bv_handle::kBranches, std::max<int>(1, (int)h->buckets.size()));
+    for (int b = 0; b < nbr_streams && e == cudaSuccess; ++b) e = cudaStreamWaitEvent(h->side[b], h->fork_ev, 0);
+    for (size_t bi = 0; bi < h->buckets.size() && e == cudaSuccess; ++bi) {
+      const Bucket& b = h->buckets[bi];
+      cudaStream_t st = h->side[bi % nbr_streams];
       if (use_v1)
-        e = bv::launch_block_v1(b.count, b.Nmax, h->stream, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset,
-                                h->d_theta, h->d_u, h->d_d, h->d_limbs, h->d_status);
+        e = bv::launch_block_v1(b.count, b.Nmax, st, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset,
+                                h->d_theta, h->d_u, h->d_d, h->d_acc, h->kb);
       else
-        e = bv::launch_block_v2(kind, b.count, b.Nmax, b.cap, h->stream, h->d_pts, h->d_nbr, h->d_desc,
+        e = bv::launch_block_v2(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
                                 h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
-                                h->d_d, h->d_limbs, h->d_status);
+                                h->d_d, h->d_acc, h->kb);
+    }
+    for (int b = 0; b < nbr_streams && e == cudaSuccess; ++b) {
+      e = cudaEventRecord(h->join_ev[b], h->side[b]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(h->stream, h->join_ev[b], 0);
     }
     if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k1, h->stream, cudaEventRecordExternal);
-    if (e == cudaSuccess) e = bv::launch_reduce(h->d_limbs, h->d_status, h->nq, h->kb, h->d_acc, h->stream);
     ncclResult_t r = ncclSuccess;
     if (e == cudaSuccess && world > 1)
       r = ncclAllReduce(h->d_acc, h->d_acc, 7, ncclUint64, ncclSum, h->comm, h->stream);
@@ -677,7 +710,7 @@ bv_status bv_last_kernel_ms(const bv_handle* h, float* ms) {
 
 int32_t bv_launches_per_eval(const bv_handle* h) {
   if (!h) return 0;
-  int32_t c = 1;  // reduction
+  int32_t c = 0;  // one kernel per non-empty bucket (the reduction is fused into them)
   for (const Bucket& b : h->buckets)
     if (b.count > 0) ++c;
   return c;

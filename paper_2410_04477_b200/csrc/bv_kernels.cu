@@ -35,8 +35,7 @@ __global__ void __launch_bounds__(NT) bv_block_v1_kernel(const PointRec* __restr
                                                          const int32_t* __restrict__ list,
                                                          const Theta* __restrict__ theta_dev,
                                                          double* __restrict__ out_u, double* __restrict__ out_d,
-                                                         uint32_t* __restrict__ limbs,
-                                                         int32_t* __restrict__ status) {
+                                                         unsigned long long* __restrict__ acc, int k_begin) {
   extern __shared__ __align__(16) double smem[];
   const int q = list[blockIdx.x];
   const BlockDesc ds = desc[q];
@@ -72,7 +71,7 @@ __global__ void __launch_bounds__(NT) bv_block_v1_kernel(const PointRec* __restr
   for (int j = 0; j < N; ++j) {
     const double* cj = A + col_off(j, Na);
     const double p = cj[0];
-    if (!(p > 0.0) || !isfinite(p)) {  // uniform across the CTA
+    if (!(p > kPivotFloor * th.sigma2) || !isfinite(p)) {  // uniform across the CTA (reading G15)
       fail = 1;
       break;
     }
@@ -101,51 +100,7 @@ __global__ void __launch_bounds__(NT) bv_block_v1_kernel(const PointRec* __restr
       out_u[q] = 0.0;
       out_d[q] = 0.0;
     }
-#pragma unroll
-    for (int i = 0; i < 6; ++i) limbs[(size_t)q * 6 + i] = c[i];
-    status[q] = st;
-  }
-}
-
-// a9. deterministic reduction over this rank's positions: integer chunk sums
-// (order-independent) + failure count + smallest failing position.
-__global__ void __launch_bounds__(1024) bv_reduce_kernel(const uint32_t* __restrict__ limbs,
-                                                         const int32_t* __restrict__ status, int nq,
-                                                         int k_begin, unsigned long long* __restrict__ acc) {
-  __shared__ unsigned long long sh[32][kAccSlots];
-  unsigned long long a[kAccSlots];
-#pragma unroll
-  for (int c = 0; c < 6; ++c) a[c] = 0ull;
-  a[6] = 0ull;
-  a[7] = ~0ull;
-  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
-#pragma unroll
-    for (int c = 0; c < 6; ++c) a[c] += limbs[(size_t)q * 6 + c];
-    if (status[q] != kOk) {
-      a[6] += 1ull;
-      const unsigned long long pos = ((unsigned long long)(k_begin + q) << 8) | (unsigned long long)status[q];
-      a[7] = a[7] < pos ? a[7] : pos;
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < 7; ++c)
-    for (int o = 16; o > 0; o >>= 1) a[c] += __shfl_xor_sync(0xffffffffu, a[c], o);
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long t = __shfl_xor_sync(0xffffffffu, a[7], o);
-    a[7] = a[7] < t ? a[7] : t;
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (lane == 0)
-    for (int c = 0; c < kAccSlots; ++c) sh[warp][c] = a[c];
-  __syncthreads();
-  if (threadIdx.x < kAccSlots) {
-    const int c = threadIdx.x;
-    unsigned long long v = (c == 7) ? ~0ull : 0ull;
-    for (int w = 0; w < nw; ++w) {
-      if (c == 7) v = v < sh[w][c] ? v : sh[w][c];
-      else v += sh[w][c];
-    }
-    acc[c] = v;
+    accumulate_term(acc, c, st, k_begin + q);  // a9
   }
 }
 
@@ -173,17 +128,11 @@ cudaError_t prepare_block_v1(int Nmax) {
 
 cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                             const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
-                            uint32_t* limbs, int32_t* status) {
+                            unsigned long long* acc, int k_begin) {
   constexpr int NT = kV1Threads;
   const size_t smem = v1_smem_bytes(Nmax);
   if (nblocks == 0) return cudaSuccess;
-  bv_block_v1_kernel<NT><<<nblocks, NT, smem, s>>>(pts, nbr, desc, list, th, u, d, limbs, status);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_reduce(const uint32_t* limbs, const int32_t* status, int nq, int k_begin,
-                          unsigned long long* acc, cudaStream_t s) {
-  bv_reduce_kernel<<<1, 1024, 0, s>>>(limbs, status, nq, k_begin, acc);
+  bv_block_v1_kernel<NT><<<nblocks, NT, smem, s>>>(pts, nbr, desc, list, th, u, d, acc, k_begin);
   return cudaGetLastError();
 }
 

@@ -29,11 +29,16 @@ def main():
     bv.loglik(theta)
     L.bv_debug_phase_cycles(buf, 0)
     ctas = buf[7]
-    warps_per_cta = {1: 1, 2: 3, 8: 3, 9: 3}
+    import re
+    src = open(os.path.join(ROOT, "paper_2410_04477_b200", "csrc", "bv_block_v2.cu")).read()
+    kw = int(re.search(r"constexpr int kW = (\d+);", src).group(1))
+    warps_per_cta = {1: 1, 2: kw - 1, 8: kw - 1, 9: kw - 1}
+    for i in (0, 3, 4, 5, 6):
+        warps_per_cta[i] = kw
     print(f"{cfg}: kernel ms {bv.last_kernel_ms():.3f}, CTAs {ctas}")
     for i in (0, 1, 2, 8, 9, 3, 4, 5, 6):
         # sums are over warps (lane 0 of each warp); report per CTA per warp-role
-        w = warps_per_cta.get(i, 4)
+        w = warps_per_cta.get(i, kw)
         print(f"  {NAMES[i]:18s} {buf[i] / ctas / w:12.0f} cycles per CTA (avg over {w} warps)")
 
 
