@@ -280,9 +280,12 @@ def main():
                 "peak_source": "derived FP64: 148 SM x 64 FMA/clk x 2 x 1.965 GHz; DMMA probe measured 37.13 "
                                "(tools/peaks)"}
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof):  # DRAM bytes (read+write) of the block kernels per evaluation, from ncu --set full
         try:
-            roofline["traffic"] = json.load(open(prof)).get(args.config)
+            tr = json.load(open(prof)).get(args.config)
+            if tr:
+                roofline["traffic"] = tr["dram_bytes_per_eval_est"]
+                roofline["traffic_source"] = tr["source"]
         except Exception:
             pass
     out = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
