@@ -59,6 +59,32 @@ __device__ __forceinline__ void sts2(double* p, double a, double b) {
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
 
+// One 8-double row (64 bytes) of a tile, moved as four 16-byte chunks in a
+// rotated order: thread row g touches chunk (k + g/2) mod 4 at step k, so the
+// 8 rows of a tile hit 8 distinct bank groups (row stride 64 B would otherwise
+// make even/odd rows collide 4-way).  Shared memory bandwidth is this
+// kernel's scarcest resource.
+__device__ __forceinline__ double2 sel4(const double2 (&v)[4], int i) {
+  const double2 a = (i & 1) ? v[1] : v[0];
+  const double2 b = (i & 1) ? v[3] : v[2];
+  return (i & 2) ? b : a;
+}
+__device__ __forceinline__ void ld_row_rot(const double* row, int rot, double2 (&ch)[4]) {
+  double2 t[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t[k] = lds2(row + 2 * ((k + rot) & 3));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) ch[q] = sel4(t, (q - rot) & 3);  // chunk q was loaded at step (q − rot) mod 4
+}
+__device__ __forceinline__ void st_row_rot(double* row, int rot, const double2 (&ch)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = (k + rot) & 3;
+    const double2 v = sel4(ch, q);
+    sts2(row + 2 * q, v.x, v.y);
+  }
+}
+
 }  // namespace
 
 #ifdef BV_PROFILE_PHASES
@@ -98,10 +124,9 @@ struct V2Layout {
 // Branch-free for the closed forms: every lane evaluates the covariance, then
 // selects (P holds 8·TI zero-padded records, so the loads are in bounds).
 template <int KIND>
-__device__ __forceinline__ double joint_entry(const PointRec* P, int r, int c, int N, const Theta& th,
-                                             const double* tab64) {
-  const PointRec pc = P[c];
-  double v = matern_kind<KIND>(sqdist(P[r], pc), th, tab64);
+__device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec& pc, int r, int c, int N,
+                                             const Theta& th, const double* tab64) {
+  double v = matern_kind<KIND>(sqdist(pr, pc), th, tab64);
   v = (r == N) ? pc.v : v;
   return (c >= N || r > N) ? 0.0 : v;
 }
@@ -123,7 +148,6 @@ __device__ __forceinline__ void factor_diag_tile(const double* tile, double* dia
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int k = 0; k <= i; ++k) a[i][k] = tile[8 * i + k];
-  double rv[8], lv[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     double p = a[j][j];
@@ -134,20 +158,27 @@ __device__ __forceinline__ void factor_diag_tile(const double* tile, double* dia
     p = (real & ok) ? p : 1.0;
     prod *= (j >= jm) ? p : 1.0;
     const double r = rsqrt_pos(p);
-    rv[j] = real ? r : 0.0;
-    lv[j] = p * r;  // L_jj = √p (≤ 1 ulp)
+    const double rv = real ? r : 0.0;
+    const double lv = p * r;  // L_jj = √p (≤ 1 ulp)
     // L_ij = a_ij / L_jj: scale by r, then one residual correction so each
     // entry is rounded on its own (a systematic per-column scale error would be
     // amplified by the ill-conditioned Schur complements of late blocks)
 #pragma unroll
     for (int i = j + 1; i < 8; ++i) {
-      const double x = a[i][j] * rv[j];
-      a[i][j] = fma(fma(-x, lv[j], a[i][j]), rv[j], x);
+      const double x = a[i][j] * rv;
+      a[i][j] = fma(fma(-x, lv, a[i][j]), rv, x);
     }
 #pragma unroll
     for (int i = j + 1; i < 8; ++i)
 #pragma unroll
       for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
+    // column j is final: publish it now (frees its registers for the rest)
+    if (lane == 0) {
+#pragma unroll
+      for (int i = j + 1; i < 8; ++i) diagL[8 * i + j] = a[i][j];
+      diagL[9 * j] = lv;  // the diagonal slots hold L_jj
+      rinv[j] = rv;
+    }
   }
 #pragma unroll
   for (int i = 1; i < 8; ++i)
@@ -156,17 +187,6 @@ __device__ __forceinline__ void factor_diag_tile(const double* tile, double* dia
       for (int k = 0; k < i; ++k)
         if (k >= jm) qd = fma(a[i][k], a[i][k], qd);
     }
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 1; i < 8; ++i)
-#pragma unroll
-      for (int k = 0; k < i; ++k) diagL[8 * i + k] = a[i][k];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      rinv[k] = rv[k];
-      diagL[9 * k] = lv[k];  // the diagonal slots hold L_jj
-    }
-  }
 }
 
 // Panel update on the tensor cores for the NS tiles I = J+1+(u−1)+3s of update
@@ -191,21 +211,43 @@ __device__ __forceinline__ void panel_gemm(double (&S0)[MAXT][2], const double* 
 }
 
 // a3: generate the row-major tiles I = I0 .. TI−1 of column panel J into their
-// slots, entries spread over `nthr` threads.  A plain loop (BV_GEN_UNROLL
-// entries in flight per thread): few copies of the Matérn code keep the kernel
-// inside the instruction cache.
+// slots: one thread per row r (8 entries, the 8 column points are the same for
+// every thread — broadcast loads — so 8 independent Matérn chains are in
+// flight per thread), each row stored with rotated 16-byte chunks.
+#ifndef BV_GEN_ROWS
+#define BV_GEN_ROWS 0
+#endif
 template <int KIND>
-__device__ __forceinline__ void gen_tiles(const PointRec* P, int N, const Theta& th, const double* tab64,
-                                          double* slots, const int16_t* tab, int TI, int I0, int J, int thr,
-                                          int nthr) {
+__device__ __forceinline__ void gen_tiles(const PointRec* P, int N, const Theta& th, const double* etab,
+                                          double* slots, const int16_t* tab, int TI, int I0, int J, int thr, int nthr) {
+#if BV_GEN_ROWS
+  const int rows = (TI - I0) * 8;
+#pragma unroll 1
+  for (int rr = thr; rr < rows; rr += nthr) {
+    const int I = I0 + (rr >> 3), g = rr & 7, r = 8 * I + g;
+    const PointRec pr = P[r];
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int c = 8 * J + k;
+      v[k] = joint_entry<KIND>(pr, P[c], r, c, N, th, etab);
+    }
+    const double2 ch[4] = {make_double2(v[0], v[1]), make_double2(v[2], v[3]), make_double2(v[4], v[5]),
+                           make_double2(v[6], v[7])};
+    st_row_rot(slots + 64 * tab[I * TI + J] + 8 * g, g >> 1, ch);
+  }
+#else
+  // one entry per thread per step, kGenUnroll steps in flight; consecutive
+  // threads take consecutive columns of a row (column points broadcast per row)
   const int total = (TI - I0) * 64;
 #pragma unroll(kGenUnroll)
   for (int e = thr; e < total; e += nthr) {
     const int I = I0 + (e >> 6);
     const int r = 8 * I + ((e >> 3) & 7);
     const int c = 8 * J + (e & 7);
-    slots[64 * tab[I * TI + J] + (e & 63)] = joint_entry<KIND>(P, r, c, N, th, tab64);
+    slots[64 * tab[I * TI + J] + (e & 63)] = joint_entry<KIND>(P[r], P[c], r, c, N, th, etab);
   }
+#endif
 }
 
 #ifndef BV_MINB
@@ -337,11 +379,14 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       const int gg = rr & 7;
       double* src = slots + 64 * tab[I * TI + J] + 8 * gg;  // C(I,J) row gg → L(I,J) row gg
       double c[8], x[8];
+      {
+        double2 ch[4];
+        ld_row_rot(src, gg >> 1, ch);
 #pragma unroll
-      for (int k = 0; k < 8; k += 2) {
-        const double2 v = lds2(src + k);
-        c[k] = v.x;
-        c[k + 1] = v.y;
+        for (int q = 0; q < 4; ++q) {
+          c[2 * q] = ch[q].x;
+          c[2 * q + 1] = ch[q].y;
+        }
       }
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
@@ -360,8 +405,11 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           if (8 * J + k >= m && 8 * J + k < N) qd = fma(x[k], x[k], qd);
         misc[1] += qd;
       }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) sts2(src + 2 * k, x[k], x[k + 4]);
+      {  // fragment order: chunk q of the row holds (L[q], L[q+4])
+        const double2 ch[4] = {make_double2(x[0], x[4]), make_double2(x[1], x[5]), make_double2(x[2], x[6]),
+                               make_double2(x[3], x[7])};
+        st_row_rot(src, gg >> 1, ch);
+      }
     }
     PH_ADD(4, t_b);
     PH_T(t_s2);

@@ -1,0 +1,561 @@
+// bv_block_v3.cu — the block kernel, warp-specialised pipeline.
+//
+// Same mathematics as bv_block_v2.cu (header there): the left-looking 8×8-tiled
+// Cholesky of the augmented joint matrix [[Σcon, Σcross, y_NN],[Σcrossᵀ, Σlk,
+// y_B]] of one block per CTA (Alg. 1 l.10-29), DMMA.8x8x4
+// panel updates, Matérn generated on the fly.  What changes is the schedule:
+// v2 ran every panel as three CTA-wide phases (diagonal factor ‖ update → row
+// solves → last update term), so each panel paid three full barriers and the
+// block's serial pivot chain waited for the bulk work every panel.  Here the
+// chain runs on its own warp and hands results to the three update warps
+// through named barriers (bar.arrive / bar.sync), one panel ahead:
+//
+//  diagonal warp D, iteration J:              update warps U (96 threads), iteration J:
+//    factor C(J,J)  → publish L_JJ, 1/L_jj      generate A(I,J+1), I ≥ J+2 (slots)
+//    sync  E  (U finished iteration J−1)         S(I) = Σ_{K<J} L(I,K) L(J+1,K)ᵀ (DMMA)
+//    arrive G                                    sync G
+//    P = A(J+1,J+1) − Σ_{K<J} L(J+1,K)L(J+1,K)ᵀ  L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2 (row solves)
+//    L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ (8 rows)         sync U-only barrier
+//    arrive F                                    sync F
+//    C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ         C(I,J+1) = A − S − L(I,J) L(J+1,J)ᵀ → slots
+//    → next J (no wait for the bulk)             arrive E
+//
+// The diagonal tile never leaves the chain warp (it lives in a private 8×8
+// buffer); every other tile lives in one slot from generation through its
+// in-place solve to its last use (slot table: bv_host.cpp SlotTables, v3
+// schedule).  Non-PD blocks keep running the protocol on substituted pivots
+// (no early exit, so no warp can be left waiting at a barrier) and are flagged.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bv_common.cuh"
+#include "matern.cuh"
+
+namespace bv {
+namespace v3 {
+
+constexpr int kW = 4;
+constexpr int kNT = kW * 32;
+constexpr int kBarG = 1, kBarF = 2, kBarE = 3, kBarU = 4, kBarH = 5;  // named barriers (0 = __syncthreads)
+
+#ifdef BV_PROFILE_PHASES
+// Debug-only phase timers, summed over warps (lane 0): chain 0 factor, 1 wait E,
+// 2 P partial, 3 row solve + F, 4 final; update 5 generation, 6 GEMM,
+// 7 wait G, 8 row solves, 9 U barrier, 10 wait F, 11 final; 12 CTAs.
+__device__ unsigned long long g_v3_cycles[16];
+#define P3_T(v) long long v = clock64()
+#define P3_ADD(i, v0)                                                                             \
+  do {                                                                                            \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_v3_cycles[i], (unsigned long long)(clock64() - (v0))); \
+  } while (0)
+#else
+#define P3_T(v)
+#define P3_ADD(i, v0)
+#endif
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void sts2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+__device__ __forceinline__ double neg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// 8-double rows moved as four 16-byte chunks in a rotated order (row g touches
+// chunk (k + g/2) mod 4 at step k): the 8 rows of a tile hit 8 distinct bank
+// groups.  Layout unchanged (chunk q at offset 2q).
+__device__ __forceinline__ double2 sel4(const double2 (&v)[4], int i) {
+  const double2 a = (i & 1) ? v[1] : v[0];
+  const double2 b = (i & 1) ? v[3] : v[2];
+  return (i & 2) ? b : a;
+}
+__device__ __forceinline__ void ld_row_rot(const double* row, int rot, double (&c)[8]) {
+  double2 t[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t[k] = lds2(row + 2 * ((k + rot) & 3));
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 v = sel4(t, (q - rot) & 3);
+    c[2 * q] = v.x;
+    c[2 * q + 1] = v.y;
+  }
+}
+// store row x in DMMA fragment order: chunk q holds (x[q], x[q+4])
+__device__ __forceinline__ void st_row_frag_rot(double* row, int rot, const double (&x)[8]) {
+  const double2 ch[4] = {make_double2(x[0], x[4]), make_double2(x[1], x[5]), make_double2(x[2], x[6]),
+                         make_double2(x[3], x[7])};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = (k + rot) & 3;
+    const double2 v = sel4(ch, q);
+    sts2(row + 2 * q, v.x, v.y);
+  }
+}
+
+struct Layout {
+  int P, dtile, ptile, dL, rinv, misc, theta, etab, slots, tab, total_bytes;
+  __host__ __device__ Layout(int TImax, int cap) {
+    P = 0;                   // PointRec[8·TImax]
+    dtile = P + 32 * TImax;  // C(J,J), row-major (chain warp only)
+    ptile = dtile + 64;      // next diagonal tile's partial P(J+1,J+1) (update warps → chain)
+    dL = ptile + 64;         // [2][64] factored diagonal tile (row-major lower, L_jj on the diagonal)
+    rinv = dL + 128;         // [2][8]  1/L_jj (0 on padding columns)
+    misc = rinv + 16;        // [1] quad (atomic), [2] fail, [3] chain warp
+    theta = misc + 8;        // Theta (≤ 20 doubles)
+    etab = theta + 20;       // 2^{−j/64}, j = 0..63 (exp_neg)
+    slots = etab + 64;       // cap tiles
+    tab = slots + 64 * cap;  // int16 slot table (TImax²)
+    total_bytes = (tab + (TImax * TImax + 3) / 4) * 8;
+  }
+};
+
+template <int KIND>
+__device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec& pc, int r, int c, int N,
+                                             const Theta& th, const double* tab64) {
+  double v = matern_kind<KIND>(sqdist(pr, pc), th, tab64);
+  v = (r == N) ? pc.v : v;
+  return (c >= N || r > N) ? 0.0 : v;
+}
+
+// Row solve x = c L_JJ⁻ᵀ against the published diagonal factor (row-major
+// lower with L_jj on the diagonal, 1/L_jj in ri): scaled by 1/L_kk, then one
+// residual correction per entry.
+__device__ __forceinline__ void row_solve(const double (&c)[8], const double* dl, const double* ri, double (&x)[8]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    double tv = c[k];
+#pragma unroll
+    for (int kk = 0; kk < k; ++kk) tv = fma(-x[kk], dl[8 * k + kk], tv);
+    const double xk = tv * ri[k];
+    x[k] = fma(fma(-xk, dl[9 * k], tv), ri[k], xk);
+  }
+}
+
+// In-lane Cholesky of the 8×8 tile t (row-major lower, every lane holds it).
+__device__ __forceinline__ void factor_tile(const double* t, double* dl, double* ri, int J, int m, int N, int lane,
+                                            double pfloor, double& prod, int& nbad, double& qd) {
+  const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
+  double a[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int k = 0; k <= i; ++k) a[i][k] = t[8 * i + k];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    double p = a[j][j];
+    const bool ok = (p > pfloor) & (p <= 1.7976931348623157e308);  // reading G15
+    const bool real = j < nreal;
+    nbad += (real & !ok) ? 1 : 0;
+    p = (real & ok) ? p : 1.0;
+    prod *= (j >= jm) ? p : 1.0;
+    const double r = rsqrt_pos(p);
+    const double rv = real ? r : 0.0;
+    const double lv = p * r;
+#pragma unroll
+    for (int i = j + 1; i < 8; ++i) {
+      const double x = a[i][j] * rv;
+      a[i][j] = fma(fma(-x, lv, a[i][j]), rv, x);
+    }
+#pragma unroll
+    for (int i = j + 1; i < 8; ++i)
+#pragma unroll
+      for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
+    if (lane == 0) {
+#pragma unroll
+      for (int i = j + 1; i < 8; ++i) dl[8 * i + j] = a[i][j];
+      dl[9 * j] = lv;
+      ri[j] = rv;
+    }
+  }
+#pragma unroll
+  for (int i = 1; i < 8; ++i)
+    if (i == yr) {
+#pragma unroll
+      for (int k = 0; k < i; ++k)
+        if (k >= jm) qd = fma(a[i][k], a[i][k], qd);
+    }
+}
+
+// Update-warp GEMM for NS tiles I = J+1+(u−1)+3s (warp 1's first tile is the
+// next diagonal tile): S(s) += Σ_{K<J} L(I,K) L(J+1,K)ᵀ.
+template <int NS, int MAXT>
+__device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
+                                       int uw, int lane) {
+  const int16_t* tJ = tab + (J + 1) * TI;
+  const int16_t* tI[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) tI[s] = tab + (J + uw + (kW - 1) * s) * TI;
+#pragma unroll 2
+  for (int K = 0; K < J; ++K) {
+    const double2 b = lds2(slots + 64 * tJ[K] + 2 * lane);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const double2 a = lds2(slots + 64 * tI[s][K] + 2 * lane);
+      dmma884(S[s][0], S[s][1], a.x, b.x);
+      dmma884(S[s][0], S[s][1], a.y, b.y);
+    }
+  }
+}
+
+#ifndef BV_MINB
+#define BV_MINB 4
+#endif
+
+template <int MAXT, int KIND>
+__global__ void __launch_bounds__(kNT, BV_MINB)
+bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__ nbr,
+                   const BlockDesc* __restrict__ desc, const int32_t* __restrict__ list,
+                   const Theta* __restrict__ theta_dev, const int16_t* __restrict__ tabs,
+                   const int32_t* __restrict__ tab_off, const double* __restrict__ exp_tab, int TImax, int cap,
+                   double* __restrict__ out_u, double* __restrict__ out_d, unsigned long long* __restrict__ acc,
+                   int k_begin) {
+  extern __shared__ __align__(16) double smem[];
+  const Layout Ly(TImax, cap);
+  const int q = list[blockIdx.x];
+  const BlockDesc ds = desc[q];
+  const int m = ds.m, l = ds.l, N = m + l;
+  const int TJ = (N + 7) >> 3;  // column panels
+  const int TI = (N + 8) >> 3;  // tile rows (incl. the y row)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+
+  PointRec* P = reinterpret_cast<PointRec*>(smem + Ly.P);
+  double* dtile = smem + Ly.dtile;
+  double* ptile = smem + Ly.ptile;
+  double* dL = smem + Ly.dL;
+  double* rinv = smem + Ly.rinv;
+  double* misc = smem + Ly.misc;
+  Theta* ths = reinterpret_cast<Theta*>(smem + Ly.theta);
+  double* etab = smem + Ly.etab;
+  double* slots = smem + Ly.slots;
+  int16_t* tab = reinterpret_cast<int16_t*>(smem + Ly.tab);
+
+  // a1/a2: θ, gathered points (neighbours first), slot table, exp table
+  if (tid < 64) etab[tid] = exp_tab[tid];
+  if (tid < (int)(sizeof(Theta) / 8))
+    reinterpret_cast<double*>(ths)[tid] = reinterpret_cast<const double*>(theta_dev)[tid];
+#pragma unroll 1
+  for (int i = tid; i < 8 * TI; i += kNT) {
+    PointRec r = {0.0, 0.0, 0.0, 0.0};
+    if (i < N) r = pts[(i < m) ? nbr[ds.nbr_off + i] : ds.pstart + (i - m)];
+    P[i] = r;
+  }
+  {
+    const int16_t* gt = tabs + tab_off[2 * TI + (TI - TJ)];
+#pragma unroll 1
+    for (int e = tid; e < TI * TI; e += kNT) tab[e] = gt[e];
+  }
+  if (tid < 4) misc[tid] = 0.0;
+  __syncthreads();
+#ifdef BV_CHAIN_SMSP0
+  {  // the chain warp is the one on SM sub-partition 0
+    unsigned wid;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+    if (lane == 0 && (wid & 3u) == 0u) misc[3] = (double)warp;
+  }
+#endif
+  // default: the chain is warp 0 — the hardware rotates co-resident CTAs'
+  // warps over the four SM sub-partitions (tools/peaks/wid_probe), so the
+  // chains of the ~4 resident blocks land on different FP64 pipes
+  const Theta& th = *ths;
+  // a3 panel 0: C(I,0) = A(I,0) for I ≥ 1 into slots; C(0,0) into dtile
+#pragma unroll 2
+  for (int e = tid; e < TI * 64; e += kNT) {
+    const int I = e >> 6, r = 8 * I + ((e >> 3) & 7), c = e & 7;
+    const double v = joint_entry<KIND>(P[r], P[c], r, c, N, th, etab);
+    if (I == 0) dtile[e] = v;
+    else slots[64 * tab[I * TI] + (e & 63)] = v;
+  }
+  __syncthreads();
+  const int cw = (int)misc[3];
+  const int uw = (warp - cw) & (kW - 1);  // 0 = chain warp, 1..3 = update warps
+  const double pfloor = kPivotFloor * th.sigma2;
+
+  if (uw == 0) {
+    // ---------------------------------------------------------- chain warp
+    double pm = 1.0, qd_in = 0.0, qd_t = 0.0;
+    int pe = 0, nbad = 0;
+    for (int J = 0; J < TJ; ++J) {
+      double* dl = dL + 64 * (J & 1);
+      double* ri = rinv + 8 * (J & 1);
+      P3_T(t0);
+      factor_tile(dtile, dl, ri, J, m, N, lane, pfloor, pm, nbad, qd_in);  // a4/a7
+      int ex;
+      pm = frexp(pm, &ex);
+      pe += ex;
+      __syncwarp();
+      P3_ADD(0, t0);
+      P3_T(t1);
+      // U finished iteration J−1 (so it has consumed G, F, H of J−1: a named
+      // barrier must not receive this warp's next arrival before its previous
+      // phase completed)
+      if (J >= 1) bar_sync(kBarE, kNT);
+      bar_arrive(kBarG, kNT);
+      P3_ADD(1, t1);
+      if (J + 1 >= TJ) {
+        // last panel: when N is a multiple of 8 the y row sits alone in tile row
+        // TJ, below the last diagonal tile — its solve is this warp's (U only
+        // handles rows I ≥ J+2)
+        if (TI > TJ && lane == (N & 7)) {
+          double c[8], x[8];
+          ld_row_rot(slots + 64 * tab[TJ * TI + J] + 8 * (N & 7), (N & 7) >> 1, c);
+          row_solve(c, dl, ri, x);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
+        }
+        break;
+      }
+      P3_T(t3);
+      // L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ: row i = lane & 7 (lanes 8..31 shadow)
+      double* row = slots + 64 * tab[(J + 1) * TI + J] + 8 * (lane & 7);
+      {
+        double c[8], x[8];
+        ld_row_rot(row, (lane & 7) >> 1, c);
+        row_solve(c, dl, ri, x);
+        if (8 * (J + 1) + (lane & 7) == N && lane < 8) {  // the y row: u += Σ_{j≥m} z_j²
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
+        }
+        __syncwarp();
+        if (lane < 8) st_row_frag_rot(row, (lane & 7) >> 1, x);
+      }
+      __syncwarp();
+      const double2 lf = lds2(slots + 64 * tab[(J + 1) * TI + J] + 2 * lane);  // read before F: slot may be recycled
+      P3_ADD(3, t3);
+      P3_T(t4);
+      bar_sync(kBarH, kNT);  // the update warps published P(J+1,J+1)
+      const double2 pp = lds2(ptile + 8 * g + 2 * t);  // read before F: U regenerates ptile after F
+      bar_arrive(kBarF, kNT);
+      // C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ → dtile
+      double p0 = pp.x, p1 = pp.y;
+      dmma884(p0, p1, neg(lf.x), lf.x);
+      dmma884(p0, p1, neg(lf.y), lf.y);
+      sts2(dtile + 8 * g + 2 * t, p0, p1);
+      __syncwarp();
+      P3_ADD(4, t4);
+    }
+    if (nbad && lane == 0) misc[2] = 1.0;
+    // y-row contributions of the chain warp: in-lane part (identical in all lanes) + row solves
+    for (int o = 16; o > 0; o >>= 1) qd_t += __shfl_xor_sync(0xffffffffu, qd_t, o);
+    if (lane == 0) {
+      atomicAdd(misc + 1, qd_in + qd_t);
+      misc[4] = log(pm) + (double)pe * 0.69314718055994530942;  // d = Σ_{j≥m} log p_j
+    }
+  } else {
+    // ---------------------------------------------------------- update warps
+    const int utid = (uw - 1) * 32 + lane;
+    double qd_u = 0.0;
+    for (int J = 0; J < TJ; ++J) {
+      const bool ahead = J + 1 < TJ;
+      double S[MAXT][2];
+#pragma unroll
+      for (int s = 0; s < MAXT; ++s) S[s][0] = S[s][1] = 0.0;
+      if (ahead) {
+        P3_T(u5);
+        // a3: A(I,J+1), I ≥ J+1 (the diagonal one into ptile, the rest into their slots)
+        const int total = (TI - J - 1) * 64;
+#pragma unroll 2
+        for (int e = utid; e < total; e += 96) {
+          const int I = J + 1 + (e >> 6), r = 8 * I + ((e >> 3) & 7), c = 8 * (J + 1) + (e & 7);
+          const double v = joint_entry<KIND>(P[r], P[c], r, c, N, th, etab);
+          if (e < 64) ptile[e] = v;
+          else slots[64 * tab[I * TI + J + 1] + (e & 63)] = v;
+        }
+        P3_ADD(5, u5);
+        P3_T(u6);
+        // partial update of this warp's tiles I = J+1+(u−1)+3s (exact count)
+        const int ns = (TI - J - 1 - (uw - 1) + (kW - 2)) / (kW - 1);
+        switch (ns) {
+#define BV_NS(n) \
+  case n:        \
+    if (MAXT >= n) u_gemm<(MAXT >= n ? n : 1), MAXT>(S, slots, tab, TI, J, uw, lane); \
+    break;
+          BV_NS(1) BV_NS(2) BV_NS(3) BV_NS(4) BV_NS(5) BV_NS(6) BV_NS(7) BV_NS(8) BV_NS(9) BV_NS(10) BV_NS(11)
+          BV_NS(12)
+#undef BV_NS
+          default: break;
+        }
+        bar_sync(kBarU, 96);  // ptile generated by all update threads
+        if (uw == 1) {        // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp
+          double* pp = ptile + 8 * g + 2 * t;
+          const double2 av = lds2(pp);
+          sts2(pp, av.x - S[0][0], av.y - S[0][1]);
+        }
+        P3_ADD(6, u6);
+      }
+      P3_T(u7);
+      bar_sync(kBarG, kNT);  // the chain warp published L_JJ
+      if (ahead) bar_arrive(kBarH, kNT);  // P(J+1,J+1) is in ptile
+      P3_ADD(7, u7);
+      P3_T(u8);
+      {
+        const double* dl = dL + 64 * (J & 1);
+        const double* ri = rinv + 8 * (J & 1);
+        const int rows = (TI - J - 2) * 8;  // L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2 (a5/a6)
+#pragma unroll 1
+        for (int rr = utid; rr < rows; rr += 96) {
+          const int I = J + 2 + (rr >> 3), gg = rr & 7;
+          double* row = slots + 64 * tab[I * TI + J] + 8 * gg;
+          double c[8], x[8];
+          ld_row_rot(row, gg >> 1, c);
+          row_solve(c, dl, ri, x);
+          if (8 * I + gg == N) {  // the y row: u += Σ_{j≥m} z_j² (a8)
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (8 * J + k >= m && 8 * J + k < N) qd_u = fma(x[k], x[k], qd_u);
+          }
+          st_row_frag_rot(row, gg >> 1, x);
+        }
+      }
+      P3_ADD(8, u8);
+      P3_T(u9);
+      bar_sync(kBarU, 96);  // all L(I,J), I ≥ J+2, visible to every update warp
+      P3_ADD(9, u9);
+      if (!ahead) continue;
+      P3_T(u10);
+      bar_sync(kBarF, kNT);  // the chain warp published L(J+1,J)
+      P3_ADD(10, u10);
+      P3_T(u11);
+      const double2 b = lds2(slots + 64 * tab[(J + 1) * TI + J] + 2 * lane);
+#pragma unroll
+      for (int s = 0; s < MAXT; ++s) {
+        const int I = J + uw + (kW - 1) * s;
+        if (I < TI && I > J + 1) {  // the diagonal tile's last term is the chain warp's
+          const double2 a = lds2(slots + 64 * tab[I * TI + J] + 2 * lane);
+          dmma884(S[s][0], S[s][1], a.x, b.x);
+          dmma884(S[s][0], S[s][1], a.y, b.y);
+          double* cp = slots + 64 * tab[I * TI + J + 1] + 8 * g + 2 * t;
+          const double2 av = lds2(cp);
+          sts2(cp, av.x - S[s][0], av.y - S[s][1]);
+        }
+      }
+      __syncwarp();
+      bar_arrive(kBarE, kNT);  // iteration J done: C(I,J+1) stored, L(·,J) final
+      P3_ADD(11, u11);
+    }
+    for (int o = 16; o > 0; o >>= 1) qd_u += __shfl_xor_sync(0xffffffffu, qd_u, o);
+    if (lane == 0 && qd_u != 0.0) atomicAdd(misc + 1, qd_u);
+  }
+  __syncthreads();
+#ifdef BV_PROFILE_PHASES
+  if (threadIdx.x == 0) atomicAdd(&g_v3_cycles[12], 1ull);
+#endif
+
+  // a8: per-block outputs and the exact fixed-point term (a9)
+  if (uw == 0 && lane == 0) {
+    const bool fail = misc[2] != 0.0;
+    int st = fail ? kNotPD : kOk;
+    uint32_t c[6] = {0, 0, 0, 0, 0, 0};
+    const double logdet = fail ? 0.0 : misc[4];
+    const double quad = fail ? 0.0 : misc[1];
+    if (!fail) {
+      const double tk = -0.5 * (quad + logdet + (double)l * kLn2Pi);
+      if (fixed_encode(tk, c)) st = kTermRange;
+    }
+    out_u[q] = quad;
+    out_d[q] = logdet;
+    accumulate_term(acc, c, st, k_begin + q);
+  }
+}
+
+}  // namespace v3
+
+// ------------------------------------------------------------------ host side
+int debug_v3_cycles(unsigned long long* out, int reset) {
+#ifdef BV_PROFILE_PHASES
+  if (out) cudaMemcpyFromSymbol(out, v3::g_v3_cycles, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(v3::g_v3_cycles, z, sizeof(z));
+  }
+  return 1;
+#else
+  (void)out;
+  (void)reset;
+  return 0;
+#endif
+}
+
+int v3_maxt_for(int TI) {
+  const int need = (TI - 1 + (v3::kW - 2)) / (v3::kW - 1);  // panel J+1 tiles I ≥ J+1 over the update warps
+  const int opts[] = {1, 2, 3, 4, 5, 6, 8, 10, 12};
+  for (int o : opts)
+    if (o >= (need < 1 ? 1 : need)) return o;
+  return -1;
+}
+
+size_t v3_smem_bytes(int TImax, int cap) { return (size_t)v3::Layout(TImax, cap).total_bytes; }
+
+template <int MAXT>
+static cudaError_t v3_prep(size_t smem) {
+  cudaError_t e = cudaSuccess;
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k) {
+    const void* f = k == 0 ? (const void*)v3::bv_block_v3_kernel<MAXT, 0>
+                  : k == 1 ? (const void*)v3::bv_block_v3_kernel<MAXT, 1>
+                  : k == 2 ? (const void*)v3::bv_block_v3_kernel<MAXT, 2>
+                           : (const void*)v3::bv_block_v3_kernel<MAXT, 3>;
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  return e;
+}
+
+cudaError_t prepare_block_v3(size_t max_smem) {
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = v3_prep<1>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<2>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<3>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<4>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<5>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<6>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<8>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<10>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<12>(max_smem);
+  return e;
+}
+
+template <int MAXT>
+static void v3_launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, const PointRec* pts,
+                           const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
+                           const int16_t* tabs, const int32_t* tab_off, const double* etab, int TImax, int cap,
+                           double* u, double* d, unsigned long long* acc, int k_begin) {
+#define BV_K(KD)                                                                                             \
+  v3::bv_block_v3_kernel<MAXT, KD><<<nblocks, v3::kNT, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, \
+                                                                  TImax, cap, u, d, acc, k_begin)
+  switch (kind) {
+    case 0: BV_K(0); break;
+    case 1: BV_K(1); break;
+    case 2: BV_K(2); break;
+    default: BV_K(3); break;
+  }
+#undef BV_K
+}
+
+cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
+                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
+                            const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
+                            unsigned long long* acc, int k_begin) {
+  if (nblocks == 0) return cudaSuccess;
+  const size_t smem = v3_smem_bytes(TImax, cap);
+  switch (v3_maxt_for(TImax)) {
+#define BV_MT(MT)                                                                                          \
+  case MT:                                                                                                 \
+    v3_launch_kind<MT>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, \
+                       acc, k_begin);                                                                      \
+    break;
+    BV_MT(1) BV_MT(2) BV_MT(3) BV_MT(4) BV_MT(5) BV_MT(6) BV_MT(8) BV_MT(10) BV_MT(12)
+#undef BV_MT
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace bv

@@ -32,7 +32,15 @@ cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRe
                             unsigned long long* acc, int k_begin);
 cudaError_t launch_scatter_y(const double* y, const int32_t* perm_of_id, int64_t n, PointRec* pts, cudaStream_t s);
 int v2_maxt_for(int TI);
+int v3_maxt_for(int TI);
+size_t v3_smem_bytes(int TImax, int cap);
+cudaError_t prepare_block_v3(size_t max_smem);
+cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
+                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
+                            const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
+                            unsigned long long* acc, int k_begin);
 int debug_phase_cycles(unsigned long long* out, int reset);
+int debug_v3_cycles(unsigned long long* out, int reset);
 size_t v2_smem_bytes(int TImax, int cap);
 cudaError_t prepare_block_v2(size_t max_smem);
 cudaError_t launch_block_v2(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
@@ -64,6 +72,10 @@ struct SlotTables {
   std::vector<int16_t> tabs;
   std::vector<int32_t> off;
   std::vector<int> cap;
+  // v3 schedule (bv_block_v3.cu): diagonal tiles never occupy a slot; column 0
+  // (I ≥ 1) first; iteration J frees row J's tiles and then generates column
+  // J+1's tiles I ≥ J+2.
+  bool v3 = true;
   void build(int TImax) {
     off.assign(2 * (size_t)(TImax + 1), 0);
     cap.assign((size_t)TImax + 1, 0);
@@ -89,12 +101,20 @@ struct SlotTables {
           --live;
           freel.push_back(v);
         };
-        for (int I = 0; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
-        for (int J = 0; J < TJ; ++J) {
-          if (J >= 1) release(t[(size_t)(J - 1) * TI + (J - 1)]);
-          for (int K = 0; K < J; ++K) release(t[(size_t)J * TI + K]);
-          if (J + 1 < TJ)
-            for (int I = J + 1; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
+        if (v3) {
+          for (int I = 1; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
+          for (int J = 0; J + 1 < TJ; ++J) {
+            for (int K = 0; K < J; ++K) release(t[(size_t)J * TI + K]);
+            for (int I = J + 2; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
+          }
+        } else {
+          for (int I = 0; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
+          for (int J = 0; J < TJ; ++J) {
+            if (J >= 1) release(t[(size_t)(J - 1) * TI + (J - 1)]);
+            for (int K = 0; K < J; ++K) release(t[(size_t)J * TI + K]);
+            if (J + 1 < TJ)
+              for (int I = J + 1; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
+          }
         }
         tabs.insert(tabs.end(), t.begin(), t.end());
         cap[TI] = std::max(cap[TI], std::max(most, 1));
@@ -126,7 +146,7 @@ struct bv_handle {
   int16_t* d_tabs = nullptr;
   double* d_exptab = nullptr;
   int32_t* d_tab_off = nullptr;
-  bool use_v1 = false;
+  bool use_v1 = false, use_v2 = false;
   bv::Theta* h_theta = nullptr;            // pinned
   unsigned long long* h_acc = nullptr;     // pinned
   cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // around the block kernels (graph event nodes)
@@ -396,8 +416,9 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     M[k] = (int32_t)(plan->nbr_ptr[k + 1] - plan->nbr_ptr[k]);
     Nmax_all = std::max(Nmax_all, L[k] + M[k]);
   }
-  const char* kenv = std::getenv("BV_KERNEL");
+  const char* kenv = std::getenv("BV_KERNEL");  // debug/A-B only: "v1" or "v2"; default v3
   const bool use_v1 = kenv && std::string(kenv) == "v1";
+  const bool use_v2 = kenv && std::string(kenv) == "v2";
   const int Nlimit = [&] {
     int N = 8;
     if (use_v1) {
@@ -405,10 +426,13 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
       return N;
     }
     SlotTables st;
+    st.v3 = !use_v2;
     st.build(48);
     while (N + 1 < 8 * 48) {
       const int TI = (N + 1 + 8) >> 3;
-      if (bv::v2_smem_bytes(TI, st.cap[TI]) > kSmemOptin || bv::v2_maxt_for(TI) < 0) break;
+      const size_t sm = use_v2 ? bv::v2_smem_bytes(TI, st.cap[TI]) : bv::v3_smem_bytes(TI, st.cap[TI]);
+      const int mt = use_v2 ? bv::v2_maxt_for(TI) : bv::v3_maxt_for(TI);
+      if (sm > kSmemOptin || mt < 0) break;
       ++N;
     }
     return N;
@@ -438,6 +462,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   h->d = d;
   h->bc = bc;
   h->use_v1 = use_v1;
+  h->use_v2 = use_v2;
   auto bail = [&](bv_status st) {
     g_setup_err = h->err;
     release(h);
@@ -509,6 +534,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     return a < b;
   });
   SlotTables slot_tables;
+  slot_tables.v3 = !use_v2;
   int TImax_all = 1;
   for (int32_t q = 0; q < h->nq; ++q) TImax_all = std::max(TImax_all, (Nq(q) + 8) >> 3);
   slot_tables.build(TImax_all);
@@ -524,7 +550,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     } else {
       const int TI = bkey(list[i]);
       h->buckets.push_back(Bucket{TI, j - i, i, slot_tables.cap[TI]});
-      max_smem = std::max(max_smem, bv::v2_smem_bytes(TI, slot_tables.cap[TI]));
+      max_smem = std::max(max_smem, use_v2 ? bv::v2_smem_bytes(TI, slot_tables.cap[TI])
+                                           : bv::v3_smem_bytes(TI, slot_tables.cap[TI]));
     }
     i = j;
   }
@@ -551,7 +578,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     TRY(upload(h, &h->d_exptab, et, 64));
   }
   if (use_v1) TRYC(bv::prepare_block_v1(maxN));
-  else TRYC(bv::prepare_block_v2(std::max<size_t>(max_smem, 1024)));
+  else if (use_v2) TRYC(bv::prepare_block_v2(std::max<size_t>(max_smem, 1024)));
+  else TRYC(bv::prepare_block_v3(std::max<size_t>(max_smem, 1024)));
 
   if (world > 1) {
     ncclUniqueId id;
@@ -591,8 +619,12 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
       if (use_v1)
         e = bv::launch_block_v1(b.count, b.Nmax, st, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset,
                                 h->d_theta, h->d_u, h->d_d, h->d_acc, h->kb);
-      else
+      else if (use_v2)
         e = bv::launch_block_v2(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
+                                h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
+                                h->d_d, h->d_acc, h->kb);
+      else
+        e = bv::launch_block_v3(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
                                 h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
                                 h->d_d, h->d_acc, h->kb);
     }
@@ -701,6 +733,7 @@ void* bv_stream(const bv_handle* h) { return h ? (void*)h->stream : nullptr; }
 
 // Debug builds only (-DBV_PROFILE_PHASES, libbv_prof.so): per-phase cycle sums.
 int bv_debug_phase_cycles(unsigned long long* out8, int reset) { return bv::debug_phase_cycles(out8, reset); }
+int bv_debug_v3_cycles(unsigned long long* out16, int reset) { return bv::debug_v3_cycles(out16, reset); }
 
 bv_status bv_last_kernel_ms(const bv_handle* h, float* ms) {
   if (!h || !ms) return BV_EINVAL;
