@@ -34,6 +34,14 @@
 namespace bv {
 namespace v3 {
 
+// Panel solve L(I,J) = C(I,J) L_JJ⁻ᵀ: 0 = row substitution (one row per
+// thread, residual-corrected divisions); 1 = DMMA with the explicit L_JJ⁻¹
+// plus one FP64 refinement step; 2 = DMMA with L_JJ⁻¹ only (A/B only: loses
+// accuracy on ill-conditioned tiles, fails the κ-aware parity rule at c3).
+#ifndef BV_TRSM
+#define BV_TRSM 1
+#endif
+
 constexpr int kW = 4;
 constexpr int kNT = kW * 32;
 constexpr int kBarG = 1, kBarF = 2, kBarE = 3, kBarU = 4, kBarH = 5;  // named barriers (0 = __syncthreads)
@@ -100,14 +108,14 @@ __device__ __forceinline__ void st_row_frag_rot(double* row, int rot, const doub
 }
 
 struct Layout {
-  int P, dtile, ptile, dL, rinv, misc, theta, etab, slots, tab, total_bytes;
+  int P, dtile, ptile, linv, lfr, misc, theta, etab, slots, tab, total_bytes;
   __host__ __device__ Layout(int TImax, int cap) {
     P = 0;                   // PointRec[8·TImax]
     dtile = P + 32 * TImax;  // C(J,J), row-major (chain warp only)
     ptile = dtile + 64;      // next diagonal tile's partial P(J+1,J+1) (update warps → chain)
-    dL = ptile + 64;         // [2][64] factored diagonal tile (row-major lower, L_jj on the diagonal)
-    rinv = dL + 128;         // [2][8]  1/L_jj (0 on padding columns)
-    misc = rinv + 16;        // [1] quad (atomic), [2] fail, [3] chain warp
+    linv = ptile + 64;       // [2][64] L_JJ⁻¹ in DMMA fragment order (0 on padding rows)
+    lfr = linv + 128;        // [2][64] L_JJ in DMMA fragment order
+    misc = lfr + 128;        // [1] chain quad, [2] fail, [3] chain warp, [4] logdet, [5..7] update-warp quads
     theta = misc + 8;        // Theta (≤ 20 doubles)
     etab = theta + 20;       // 2^{−j/64}, j = 0..63 (exp_neg)
     slots = etab + 64;       // cap tiles
@@ -138,11 +146,16 @@ __device__ __forceinline__ void row_solve(const double (&c)[8], const double* dl
   }
 }
 
-// In-lane Cholesky of the 8×8 tile t (row-major lower, every lane holds it).
-__device__ __forceinline__ void factor_tile(const double* t, double* dl, double* ri, int J, int m, int N, int lane,
+// In-lane Cholesky of the 8×8 tile t (row-major lower, every lane holds it),
+// then (BV_TRSM ≥ 1) L_JJ⁻¹ by columns (lane j solves L x = e_j).  Lanes 0..7 publish column
+// j of both L_JJ (lf) and L_JJ⁻¹ (li) in DMMA fragment order: element (i,k) at
+// 2(4i + (k&3)) + (k>>2).  Padding pivots (j ≥ N − 8J) get 1/L_jj = 0, so
+// their rows of L_JJ⁻¹ — and with them the padding columns of every
+// L(I,J) = C(I,J) L_JJ⁻ᵀ — are zero.
+__device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, int J, int m, int N, int lane,
                                             double pfloor, double& prod, int& nbad, double& qd) {
   const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
-  double a[8][8];
+  double a[8][8], rr[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -158,6 +171,8 @@ __device__ __forceinline__ void factor_tile(const double* t, double* dl, double*
     const double r = rsqrt_pos(p);
     const double rv = real ? r : 0.0;
     const double lv = p * r;
+    rr[j] = rv;
+    a[j][j] = lv;
 #pragma unroll
     for (int i = j + 1; i < 8; ++i) {
       const double x = a[i][j] * rv;
@@ -167,12 +182,6 @@ __device__ __forceinline__ void factor_tile(const double* t, double* dl, double*
     for (int i = j + 1; i < 8; ++i)
 #pragma unroll
       for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
-    if (lane == 0) {
-#pragma unroll
-      for (int i = j + 1; i < 8; ++i) dl[8 * i + j] = a[i][j];
-      dl[9 * j] = lv;
-      ri[j] = rv;
-    }
   }
 #pragma unroll
   for (int i = 1; i < 8; ++i)
@@ -181,6 +190,114 @@ __device__ __forceinline__ void factor_tile(const double* t, double* dl, double*
       for (int k = 0; k < i; ++k)
         if (k >= jm) qd = fma(a[i][k], a[i][k], qd);
     }
+  const int j = lane & 7;
+#if BV_TRSM == 0
+  // substitution mode: lf = L_JJ row-major (L_jj on the diagonal), li[0..7] = 1/L_jj
+  if (lane < 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double l = 0.0;
+#pragma unroll
+      for (int k = 0; k <= i; ++k) l = (k == j) ? a[i][k] : l;
+      lf[8 * i + j] = l;
+    }
+    double r = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r = (k == j) ? rr[k] : r;
+    li[j] = r;
+  }
+#else
+  // column j = lane & 7 of L⁻¹: x_i = (δ_ij − Σ_{k<i} L_ik x_k) / L_ii
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) s = fma(-a[i][k], x[k], s);
+    x[i] = s * rr[i];
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int o = 2 * (4 * i + (j & 3)) + (j >> 2);
+      li[o] = x[i];
+      double l = 0.0;
+#pragma unroll
+      for (int k = 0; k <= i; ++k) l = (k == j) ? a[i][k] : l;
+      lf[o] = l;
+    }
+  }
+#endif
+}
+
+// L(I,J) = C(I,J) L_JJ⁻ᵀ for one tile, in place (one warp): C is row-major,
+// the result is stored in DMMA fragment order.  bi / bl = this lane's
+// fragments of L_JJ⁻¹ / L_JJ (the B operands (L⁻ᵀ)[k][n], (Lᵀ)[k][n] at k = t,
+// n = g).  X₁ = C L⁻ᵀ, then one refinement step X = X₁ + (C − X₁Lᵀ) L⁻ᵀ with
+// the residual in FP64: this restores the accuracy of substitution, which a
+// bare multiply by the explicit inverse loses on ill-conditioned L_JJ.
+// Returns the lane's two results (row g, columns 2t, 2t+1) for the y-row term.
+template <int NT>
+__device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 bi, double2 bl, int g, int t,
+                                            double2 (&out)[NT]) {
+  double x0[NT], x1[NT], cc0[NT], cc1[NT];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const double* ra = tile[i] + 8 * g + t;  // A operand (row g, k = t / t+4) of a row-major tile
+    const double c0 = ra[0], c1 = ra[4];
+    const double2 cc = lds2(tile[i] + 8 * g + 2 * t);  // accumulator (row g, columns 2t, 2t+1)
+    cc0[i] = cc.x;
+    cc1[i] = cc.y;
+    x0[i] = x1[i] = 0.0;
+    dmma884(x0[i], x1[i], c0, bi.x);
+    dmma884(x0[i], x1[i], c1, bi.y);
+  }
+  __syncwarp();
+#if BV_TRSM == 1
+#pragma unroll
+  for (int i = 0; i < NT; ++i) sts2(tile[i] + 8 * g + 2 * t, x0[i], x1[i]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const double* ra = tile[i] + 8 * g + t;
+    dmma884(cc0[i], cc1[i], neg(ra[0]), bl.x);  // R = C − X₁ Lᵀ
+    dmma884(cc0[i], cc1[i], neg(ra[4]), bl.y);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < NT; ++i) sts2(tile[i] + 8 * g + 2 * t, cc0[i], cc1[i]);
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    const double* ra = tile[i] + 8 * g + t;
+    dmma884(x0[i], x1[i], ra[0], bi.x);  // X = X₁ + R L⁻ᵀ
+    dmma884(x0[i], x1[i], ra[4], bi.y);
+  }
+  __syncwarp();
+#else
+  (void)bl;
+  (void)cc0;
+  (void)cc1;
+#endif
+#pragma unroll
+  for (int i = 0; i < NT; ++i) {
+    tile[i][8 * g + 2 * ((2 * t) & 3) + (t >> 1)] = x0[i];
+    tile[i][8 * g + 2 * ((2 * t + 1) & 3) + (t >> 1)] = x1[i];
+    out[i] = make_double2(x0[i], x1[i]);
+  }
+}
+__device__ __forceinline__ double2 tile_trsm(double* tile, double2 bi, double2 bl, int g, int t) {
+  double* const tl[1] = {tile};
+  double2 o[1];
+  tile_trsm_n<1>(tl, bi, bl, g, t, o);
+  return o[0];
+}
+
+// y-row term of one tile solve: u += Σ_{j ≥ m, j < N} z_j² over this lane's two columns
+__device__ __forceinline__ double yrow_sq(double2 d, int J, int t, int m, int N) {
+  const int k0 = 8 * J + 2 * t, k1 = k0 + 1;
+  double q = (k0 >= m && k0 < N) ? d.x * d.x : 0.0;
+  return (k1 >= m && k1 < N) ? fma(d.y, d.y, q) : q;
 }
 
 // Update-warp GEMM for NS tiles I = J+1+(u−1)+3s (warp 1's first tile is the
@@ -203,6 +320,12 @@ __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots
     }
   }
 }
+
+
+#ifndef BV_V3_GEN_UNROLL
+#define BV_V3_GEN_UNROLL 1
+#endif
+constexpr int kV3GenUnroll = BV_V3_GEN_UNROLL;  // half-tiles in flight per update warp
 
 #ifndef BV_MINB
 #define BV_MINB 4
@@ -229,8 +352,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   PointRec* P = reinterpret_cast<PointRec*>(smem + Ly.P);
   double* dtile = smem + Ly.dtile;
   double* ptile = smem + Ly.ptile;
-  double* dL = smem + Ly.dL;
-  double* rinv = smem + Ly.rinv;
+  double* linv = smem + Ly.linv;
+  double* lfr = smem + Ly.lfr;
   double* misc = smem + Ly.misc;
   Theta* ths = reinterpret_cast<Theta*>(smem + Ly.theta);
   double* etab = smem + Ly.etab;
@@ -283,14 +406,18 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     double pm = 1.0, qd_in = 0.0, qd_t = 0.0;
     int pe = 0, nbad = 0;
     for (int J = 0; J < TJ; ++J) {
-      double* dl = dL + 64 * (J & 1);
-      double* ri = rinv + 8 * (J & 1);
+      double* li = linv + 64 * (J & 1);
+      double* lj = lfr + 64 * (J & 1);
       P3_T(t0);
-      factor_tile(dtile, dl, ri, J, m, N, lane, pfloor, pm, nbad, qd_in);  // a4/a7
+      factor_tile(dtile, lj, li, J, m, N, lane, pfloor, pm, nbad, qd_in);  // a4/a7
       int ex;
       pm = frexp(pm, &ex);
       pe += ex;
       __syncwarp();
+#if BV_TRSM != 0
+      const double2 bi = lds2(li + 2 * lane);  // this lane's fragments of L_JJ⁻¹ and L_JJ
+      const double2 bl = lds2(lj + 2 * lane);
+#endif
       P3_ADD(0, t0);
       P3_T(t1);
       // U finished iteration J−1 (so it has consumed G, F, H of J−1: a named
@@ -302,24 +429,33 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       if (J + 1 >= TJ) {
         // last panel: when N is a multiple of 8 the y row sits alone in tile row
         // TJ, below the last diagonal tile — its solve is this warp's (U only
-        // handles rows I ≥ J+2)
-        if (TI > TJ && lane == (N & 7)) {
-          double c[8], x[8];
-          ld_row_rot(slots + 64 * tab[TJ * TI + J] + 8 * (N & 7), (N & 7) >> 1, c);
-          row_solve(c, dl, ri, x);
+        // handles tiles I ≥ J+2)
+        if (TI > TJ) {
+#if BV_TRSM == 0
+          if (lane == (N & 7)) {
+            double c[8], x[8];
+            ld_row_rot(slots + 64 * tab[TJ * TI + J] + 8 * (N & 7), (N & 7) >> 1, c);
+            row_solve(c, lj, li, x);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
+            for (int k = 0; k < 8; ++k)
+              if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
+          }
+#else
+          const double2 d = tile_trsm(slots + 64 * tab[TJ * TI + J], bi, bl, g, t);
+          if (g == (N & 7)) qd_t += yrow_sq(d, J, t, m, N);
+#endif
         }
         break;
       }
       P3_T(t3);
-      // L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ: row i = lane & 7 (lanes 8..31 shadow)
-      double* row = slots + 64 * tab[(J + 1) * TI + J] + 8 * (lane & 7);
+      // L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ (a5/a6)
+      double* tj = slots + 64 * tab[(J + 1) * TI + J];
       {
+#if BV_TRSM == 0
+        double* row = tj + 8 * (lane & 7);  // row i = lane & 7 (lanes 8..31 shadow)
         double c[8], x[8];
         ld_row_rot(row, (lane & 7) >> 1, c);
-        row_solve(c, dl, ri, x);
+        row_solve(c, lj, li, x);
         if (8 * (J + 1) + (lane & 7) == N && lane < 8) {  // the y row: u += Σ_{j≥m} z_j²
 #pragma unroll
           for (int k = 0; k < 8; ++k)
@@ -327,9 +463,13 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         }
         __syncwarp();
         if (lane < 8) st_row_frag_rot(row, (lane & 7) >> 1, x);
+#else
+        const double2 d = tile_trsm(tj, bi, bl, g, t);
+        if (8 * (J + 1) + g == N) qd_t += yrow_sq(d, J, t, m, N);  // the y row: u += Σ_{j≥m} z_j²
+#endif
       }
       __syncwarp();
-      const double2 lf = lds2(slots + 64 * tab[(J + 1) * TI + J] + 2 * lane);  // read before F: slot may be recycled
+      const double2 lf = lds2(tj + 2 * lane);  // read before F: slot may be recycled
       P3_ADD(3, t3);
       P3_T(t4);
       bar_sync(kBarH, kNT);  // the update warps published P(J+1,J+1)
@@ -347,12 +487,11 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     // y-row contributions of the chain warp: in-lane part (identical in all lanes) + row solves
     for (int o = 16; o > 0; o >>= 1) qd_t += __shfl_xor_sync(0xffffffffu, qd_t, o);
     if (lane == 0) {
-      atomicAdd(misc + 1, qd_in + qd_t);
+      misc[1] = qd_in + qd_t;  // per-warp partials, summed in a fixed order below (bitwise reproducible)
       misc[4] = log(pm) + (double)pe * 0.69314718055994530942;  // d = Σ_{j≥m} log p_j
     }
   } else {
     // ---------------------------------------------------------- update warps
-    const int utid = (uw - 1) * 32 + lane;
     double qd_u = 0.0;
     for (int J = 0; J < TJ; ++J) {
       const bool ahead = J + 1 < TJ;
@@ -361,14 +500,25 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       for (int s = 0; s < MAXT; ++s) S[s][0] = S[s][1] = 0.0;
       if (ahead) {
         P3_T(u5);
-        // a3: A(I,J+1), I ≥ J+1 (the diagonal one into ptile, the rest into their slots)
-        const int total = (TI - J - 1) * 64;
-#pragma unroll 2
-        for (int e = utid; e < total; e += 96) {
-          const int I = J + 1 + (e >> 6), r = 8 * I + ((e >> 3) & 7), c = 8 * (J + 1) + (e & 7);
-          const double v = joint_entry<KIND>(P[r], P[c], r, c, N, th, etab);
-          if (e < 64) ptile[e] = v;
-          else slots[64 * tab[I * TI + J + 1] + (e & 63)] = v;
+        // a3: A(I,J+1), I ≥ J+1 (the diagonal one into ptile, the rest into
+        // their slots), by half-tiles h (rows 4(h&1)..+3 of tile I = J+1+h/2)
+        // dealt round-robin to the update warps.  A lane's column c is fixed,
+        // so its point, its validity and its in-tile offset are loop-invariant;
+        // a half-tile is 32 consecutive doubles of the row-major tile.
+        {
+          const int c = 8 * (J + 1) + (lane & 7);
+          const PointRec pc = P[c];
+          const bool cval = c < N;
+          const int nh = 2 * (TI - J - 1);
+#pragma unroll(kV3GenUnroll)
+          for (int h = uw - 1; h < nh; h += kW - 1) {
+            const int I = J + 1 + (h >> 1), r = 8 * I + 4 * (h & 1) + (lane >> 3);
+            double v = matern_kind<KIND>(sqdist(P[r], pc), th, etab);
+            v = (r == N) ? pc.v : v;
+            v = (cval && r <= N) ? v : 0.0;
+            double* dst = (h < 2) ? ptile : slots + 64 * tab[I * TI + J + 1];
+            dst[32 * (h & 1) + lane] = v;
+          }
         }
         P3_ADD(5, u5);
         P3_T(u6);
@@ -398,9 +548,12 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       P3_ADD(7, u7);
       P3_T(u8);
       {
-        const double* dl = dL + 64 * (J & 1);
-        const double* ri = rinv + 8 * (J & 1);
-        const int rows = (TI - J - 2) * 8;  // L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2 (a5/a6)
+#if BV_TRSM == 0
+        // L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2, one row per update thread (a5/a6)
+        const double* dl = lfr + 64 * (J & 1);
+        const double* ri = linv + 64 * (J & 1);
+        const int rows = (TI - J - 2) * 8;
+        const int utid = (uw - 1) * 32 + lane;
 #pragma unroll 1
         for (int rr = utid; rr < rows; rr += 96) {
           const int I = J + 2 + (rr >> 3), gg = rr & 7;
@@ -415,11 +568,30 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           }
           st_row_frag_rot(row, gg >> 1, x);
         }
+#else
+        // L(I,J) = C(I,J) L_JJ⁻ᵀ for this warp's tiles I = J+u+3s > J+1 (a5/a6)
+        const double2 bi = lds2(linv + 64 * (J & 1) + 2 * lane);
+        const double2 bl = lds2(lfr + 64 * (J & 1) + 2 * lane);
+        // two tiles in flight: their DMMA / shared-memory round trips interleave
+#pragma unroll 1
+        for (int I = J + uw + (uw == 1 ? kW - 1 : 0); I < TI; I += 2 * (kW - 1)) {
+          const int I2 = I + kW - 1;
+          if (I2 < TI) {
+            double* const tl[2] = {slots + 64 * tab[I * TI + J], slots + 64 * tab[I2 * TI + J]};
+            double2 d[2];
+            tile_trsm_n<2>(tl, bi, bl, g, t, d);
+            if (8 * I + g == N) qd_u += yrow_sq(d[0], J, t, m, N);  // the y row (a8)
+            if (8 * I2 + g == N) qd_u += yrow_sq(d[1], J, t, m, N);
+          } else {
+            const double2 d = tile_trsm(slots + 64 * tab[I * TI + J], bi, bl, g, t);
+            if (8 * I + g == N) qd_u += yrow_sq(d, J, t, m, N);
+          }
+        }
+#endif
       }
       P3_ADD(8, u8);
-      P3_T(u9);
-      bar_sync(kBarU, 96);  // all L(I,J), I ≥ J+2, visible to every update warp
-      P3_ADD(9, u9);
+      // (no U barrier here: F below is a full barrier of the update warps, so
+      // every L(I,J) is visible to all of them before the next GEMM)
       if (!ahead) continue;
       P3_T(u10);
       bar_sync(kBarF, kNT);  // the chain warp published L(J+1,J)
@@ -443,7 +615,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       P3_ADD(11, u11);
     }
     for (int o = 16; o > 0; o >>= 1) qd_u += __shfl_xor_sync(0xffffffffu, qd_u, o);
-    if (lane == 0 && qd_u != 0.0) atomicAdd(misc + 1, qd_u);
+    if (lane == 0) misc[4 + uw] = qd_u;
   }
   __syncthreads();
 #ifdef BV_PROFILE_PHASES
@@ -456,7 +628,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     int st = fail ? kNotPD : kOk;
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     const double logdet = fail ? 0.0 : misc[4];
-    const double quad = fail ? 0.0 : misc[1];
+    const double quad = fail ? 0.0 : ((misc[1] + misc[5]) + misc[6]) + misc[7];
     if (!fail) {
       const double tk = -0.5 * (quad + logdet + (double)l * kLn2Pi);
       if (fixed_encode(tk, c)) st = kTermRange;

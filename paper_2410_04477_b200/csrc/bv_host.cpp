@@ -73,8 +73,8 @@ struct SlotTables {
   std::vector<int32_t> off;
   std::vector<int> cap;
   // v3 schedule (bv_block_v3.cu): diagonal tiles never occupy a slot; column 0
-  // (I ≥ 1) first; iteration J frees row J's tiles and then generates column
-  // J+1's tiles I ≥ J+2.
+  // (I ≥ 1) first; iteration J frees row J's tiles except L(J,J−1), plus
+  // L(J−1,J−2), and then generates column J+1's tiles I ≥ J+2.
   bool v3 = true;
   void build(int TImax) {
     off.assign(2 * (size_t)(TImax + 1), 0);
@@ -104,7 +104,12 @@ struct SlotTables {
         if (v3) {
           for (int I = 1; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
           for (int J = 0; J + 1 < TJ; ++J) {
-            for (int K = 0; K < J; ++K) release(t[(size_t)J * TI + K]);
+            // L(J,J−1) is the b operand of iteration J−1's final term, which a
+            // slow update warp may still be reading while a fast one generates
+            // column J+1: it is released one iteration later (after the U
+            // barrier of iteration J has separated the two)
+            for (int K = 0; K + 1 < J; ++K) release(t[(size_t)J * TI + K]);
+            if (J >= 2) release(t[(size_t)(J - 1) * TI + J - 2]);
             for (int I = J + 2; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
           }
         } else {

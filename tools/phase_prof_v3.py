@@ -8,9 +8,9 @@ sys.path.insert(0, ROOT)
 import bvgen  # noqa: E402
 import paper_2410_04477_b200 as bvl  # noqa: E402
 
-NAMES = ["chain: factor", "chain: wait E + arrive G", "chain: P partial", "chain: row solve + F", "chain: final",
-         "upd: generation", "upd: GEMM", "upd: wait G", "upd: row solves", "upd: U barrier", "upd: wait F",
-         "upd: final + E"]
+NAMES = ["chain: factor", "chain: wait E + arrive G", "(unused)", "chain: row solve", "chain: wait H + F + final",
+         "upd: generation", "upd: GEMM + P", "upd: wait G + arrive H", "upd: row solves", "upd: U barrier",
+         "upd: wait F", "upd: final + E"]
 
 
 def main():
