@@ -327,12 +327,17 @@ __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots
 #endif
 constexpr int kV3GenUnroll = BV_V3_GEN_UNROLL;  // half-tiles in flight per update warp
 
-#ifndef BV_MINB
-#define BV_MINB 4
+// CTAs per SM the register allocation targets: shared memory admits 5 blocks
+// of TI ≤ 16 (MAXT ≤ 5, the bulk of c3/c4) and 4 of TI 17-18; 5 × 128 threads
+// caps registers at 102 (a few spills in the chain warp's in-lane factor,
+// measured +2.5 % at c4 over 4 CTAs with none).
+#ifndef BV_MINB_SMALL
+#define BV_MINB_SMALL 5
 #endif
+constexpr int v3_minb(int maxt) { return maxt <= 5 ? BV_MINB_SMALL : 4; }
 
 template <int MAXT, int KIND>
-__global__ void __launch_bounds__(kNT, BV_MINB)
+__global__ void __launch_bounds__(kNT, v3_minb(MAXT))
 bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__ nbr,
                    const BlockDesc* __restrict__ desc, const int32_t* __restrict__ list,
                    const Theta* __restrict__ theta_dev, const int16_t* __restrict__ tabs,
