@@ -149,7 +149,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     c = workload(args.config)
-    plan = bvgen.cached_plan(args.config)
+    plan = bvgen.cached_plan(args.config, m=args.m)
     theta = tuple(c["theta"])
     import oracle
     oracle.build()
@@ -165,6 +165,106 @@ def run_reference(args):
            "data": "synthetic", "config": config_block(args, c, plan),
            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "oracle", "sample": desc},
            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def ablation_leg(args):
+    """Run this script as a child with the ablation library; returns its mean kernel ms (or None)."""
+    from paper_2410_04477_b200 import build as bvbuild
+    try:
+        libp = bvbuild.build_ablation()
+        env = dict(os.environ, BV_LIB_PATH=libp)
+        cmd = [sys.executable, os.path.abspath(__file__), "--ablation-child", "--config", args.config,
+               "--steps", str(max(5, args.steps))] + (["--m", str(args.m)] if args.m else [])
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+        return float(json.loads(r.stdout.strip().splitlines()[-1])["kernel_ms"])
+    except Exception as e:  # the ablation is a diagnostic: never fail the bench line
+        print(f"ablation leg failed: {e!r}", file=sys.stderr)
+        return None
+
+
+def run_ablation_child(args):
+    import torch
+    import paper_2410_04477_b200 as bvl
+    c = workload(args.config)
+    plan = bvgen.cached_plan(args.config, m=args.m)
+    theta = tuple(c["theta"])
+    bv = bvl.BlockVecchia(plan, device=0)
+    for _ in range(3):
+        bv.loglik(theta)
+    torch.cuda.synchronize()
+    ks = []
+    for _ in range(args.steps):
+        bv.loglik(theta)
+        ks.append(bv.last_kernel_ms())
+    bv.close()
+    print(json.dumps({"kernel_ms": float(np.mean(ks))}))
+    return 0
+
+
+def synth_gp_y(plan, theta, seed):
+    """Exact zero-mean Matérn GRF draw at the plan's locations (c2 recipe: dense
+    Cholesky of the n×n covariance, a generator step — torch FP64 on the GPU, not the product
+    path).  Closed-form ν only."""
+    import torch
+    X = torch.from_numpy(plan.locs).cuda()
+    r = torch.cdist(X, X) / theta[1]
+    nu = theta[2]
+    poly = {0.5: 1.0, 1.5: 1.0 + r, 2.5: 1.0 + r + r * r / 3.0}[nu]
+    S = theta[0] * poly * torch.exp(-r)
+    del r
+    Lc = torch.linalg.cholesky(S)
+    del S
+    eps = torch.from_numpy(bvgen.normal(seed, plan.n)).cuda()
+    y = (Lc @ eps).cpu().numpy()
+    del Lc
+    torch.cuda.empty_cache()
+    return y
+
+
+def run_mle(args):
+    """c2: one MLE fit: start (0.5, 0.1, 1.0), box [0.05,5]×[0.005,0.5]×[0.2,3],
+    relative Δℓ < 1e-7 or 2000 evaluations; ν estimated, so nearly every evaluation takes the
+    general-K_ν path.  value = evaluations per second over the whole fit (optimiser included)."""
+    import torch
+    import paper_2410_04477_b200 as bvl
+    from paper_2410_04477_b200.mle import fit
+    from paper_2410_04477_b200 import build as bvbuild
+    args.config = "c2"
+    torch.cuda.set_device(0)
+    bvbuild.build()
+    c = workload("c2")
+    theta_true = tuple(c["theta"])
+    plan = bvgen.cached_plan("c2")
+    plan = plan.with_y(synth_gp_y(plan, theta_true, 100 * c["cfg"] + 2))
+    bv = bvl.BlockVecchia(plan, device=0)
+    for _ in range(3):
+        bv.loglik(theta_true)
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        res = fit(bv.loglik)
+    kern = bv.last_kernel_ms()
+    bv.close()
+    out = {"metric": "block-Vecchia MLE fit: loglik evals/sec over a full BOBYQA-style fit (c2)",
+           "value": res["evals_per_s"], "unit": "evals/s", "n_gpus": 1, "steps": res["n_evals"], "warmup": 3,
+           "ms_per_step": 1000.0 * res["wall_s"] / res["n_evals"], "higher_is_better": True, "scaling": "none",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (exact Matern GRF, dense Cholesky)",
+           "config": dict(config_block(args, c, plan), workload="c2 MLE: n=20,000 2D, bc=500, m=60, "
+                          "theta_true=(1.0, 0.052537, 1.5), start (0.5, 0.1, 1.0), nu estimated"),
+           "mle": {"theta_hat": res["theta"], "loglik_hat": res["loglik"], "n_evals": res["n_evals"],
+                   "wall_s": res["wall_s"], "converged": res["converged"], "theta_true": theta_true,
+                   "last_kernel_ms": kern},
+           "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        t = time.perf_counter()
+        ro = fit(lambda th: oracle.bv_loglik(plan, th, per_block=False)["loglik"])
+        w = time.perf_counter() - t
+        out["cpu_baseline"] = {"value": ro["n_evals"] / w, "unit": "evals/s", "cores": os.cpu_count() or 1,
+                               "kind": "oracle", "sample": "the same full MLE fit on the CPU oracle",
+                               "theta_hat": ro["theta"], "n_evals": ro["n_evals"], "seconds": w}
     print(json.dumps(out))
     return 0
 
@@ -185,9 +285,17 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(bvgen.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--m", type=int, default=None, help="override the config's m (c5 sweep: 30/60/120/200)")
+    ap.add_argument("--no-ablation", action="store_true", help="skip the factorisation-only ablation leg")
+    ap.add_argument("--ablation-child", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--mle", action="store_true", help="c2 workload: a full MLE fit (hundreds of evaluations)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.ablation_child:
+        return run_ablation_child(args)
+    if args.mle:
+        return run_mle(args)
 
     import torch
     import paper_2410_04477_b200 as bvl
@@ -206,11 +314,11 @@ def main():
     if dist:
         dist.barrier()
     c = workload(args.config)
-    plan = bvgen.cached_plan(args.config) if rank == 0 else None
+    plan = bvgen.cached_plan(args.config, m=args.m) if rank == 0 else None
     if dist:
         dist.barrier()
         if rank != 0:
-            plan = bvgen.cached_plan(args.config)
+            plan = bvgen.cached_plan(args.config, m=args.m)
     theta_a = tuple(c["theta"])
     theta_b = (theta_a[0] * 1.05, theta_a[1] * 0.97, theta_a[2])
     nid = None
@@ -298,6 +406,15 @@ def main():
                    "d2h_bytes_per_step": 64},
            "gpu_launches": int(bv.launches_per_eval * args.steps),
            "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_ablation:
+        ab = ablation_leg(args)
+        if ab is not None:
+            out["factorization_only"] = {
+                "what": "SURVEY 8d (v): the same block kernels with the Matern fill replaced by a cheap SPD fill "
+                        "(libbv_fill.so, -DBV_ABL_FILL); F / kernel time = FP64 factorisation rate",
+                "kernel_ms": ab, "achieved": F_local / (ab / 1000.0) / 1e12, "unit": "TFLOP/s",
+                "frac": F_local / (ab / 1000.0) / 1e12 / FP64_PEAK_TFLOPS,
+                "generation_ms_est": kmean - ab}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rates, desc, times, cores = oracle_sample_time(plan, theta_a, target_s=15.0)
         out["cpu_baseline"] = {"value": rates[0], "unit": "evals/s", "cores": cores, "kind": "oracle",

@@ -239,3 +239,59 @@ def cached_plan(name: str, m=None, cache_dir=None, **kw) -> Plan:
              name=p.name, m=p.m)
     os.replace(tmp, path)
     return p
+
+
+# --------------------------------------------------------- prediction plans (Alg. 2)
+@dataclasses.dataclass
+class PredPlan:
+    """Inputs of Alg. 2 for n_new new locations: the clustering g of
+    l.4 (block_id) and the NN sets of l.6 (CSR by prediction block; training ids)."""
+    locs_new: np.ndarray
+    block_id: np.ndarray
+    nbr_ptr: np.ndarray
+    nbr_idx: np.ndarray
+    m: int = 0
+
+    @property
+    def n_new(self):
+        return int(self.locs_new.shape[0])
+
+    @property
+    def bc_new(self):
+        return int(self.nbr_ptr.shape[0] - 1)
+
+
+def pred_nn(train_locs, centroids, m: int) -> tuple[np.ndarray, np.ndarray]:
+    """Per prediction-block centroid, the m nearest TRAINING points ("m nearest
+    neighbor observations from y"), ascending (squared distance summed in x, y, z order, id).
+    Candidates come from a k-d tree query with 16 spare slots, then an exact re-sort."""
+    from scipy.spatial import cKDTree
+    train_locs = np.ascontiguousarray(train_locs, dtype=np.float64)
+    n = train_locs.shape[0]
+    m = int(min(m, n))
+    bc = centroids.shape[0]
+    ptr = np.arange(bc + 1, dtype=np.int64) * m
+    if m == 0:
+        return ptr, np.zeros(0, dtype=np.int32)
+    k = min(n, m + 16)
+    _, cand = cKDTree(train_locs).query(centroids, k=k)
+    cand = np.asarray(cand).reshape(bc, k)
+    idx = np.zeros(bc * m, dtype=np.int32)
+    for b in range(bc):
+        c = cand[b]
+        diff = train_locs[c] - centroids[b]
+        d2 = diff[:, 0] * diff[:, 0]
+        for j in range(1, diff.shape[1]):
+            d2 = d2 + diff[:, j] * diff[:, j]
+        o = np.lexsort((c, d2))[:m]
+        idx[b * m:(b + 1) * m] = c[o]
+    return ptr, idx
+
+
+def make_pred_plan(train_locs, locs_new, bc_new: int, m: int, seed: int = 9003, kmeans_iter: int = 20) -> PredPlan:
+    """Alg. 2 l.4-6: K-means of the new locations into bc_new blocks, then m training NN per block
+    centroid (block mean of its points)."""
+    locs_new = np.ascontiguousarray(locs_new, dtype=np.float64)
+    bid, cent, _ = kmeans(locs_new, int(bc_new), seed, kmeans_iter)
+    ptr, idx = pred_nn(train_locs, cent, m)
+    return PredPlan(locs_new, bid.astype(np.int32), ptr, idx, int(m))

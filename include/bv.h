@@ -116,6 +116,39 @@ bv_status bv_owned_range(const bv_handle* h, int32_t* k_begin, int32_t* k_end);
  * evaluates.  Used to time the whole path with host↔device traffic. */
 bv_status bv_loglik_host_y(bv_handle* h, const double* y, const double theta[3], double* loglik);
 
+/* ---- block-Vecchia prediction (Alg. 2; §2.3 :194-240) ----
+ *
+ * New locations S* are clustered into prediction blocks B*_1..B*_bc (l.4) and
+ * every block conditions on m_i training points (l.6, any training point —
+ * "m nearest neighbor observations from y").  For each block:
+ *   μ_B* = Σcrossᵀ Σcon⁻¹ y_NN,   Σ_B* = Σlk − Σcrossᵀ Σcon⁻¹ Σcross      (l.10-11)
+ * with Σcon = K(s_NN, s_NN), Σcross = K(s_NN, s_B*) (m×l, reading G8),
+ * Σlk = K(s_B*, s_B*) and K the Matérn of Eq. (7).  y is the handle's current
+ * y (the plan's, or the last bv_loglik_host_y's).  All pointers HOST memory,
+ * borrowed for the call. */
+typedef struct {
+  int64_t n_new;            /* number of new locations, ≥ 1 */
+  const double* locs_new;   /* n_new*d row-major (d of the handle's plan), finite */
+  int32_t bc_new;           /* number of prediction blocks, ≥ 1 */
+  const int32_t* block_id;  /* n_new, in [0, bc_new), every block non-empty; a block's points are
+                               taken in ascending new-point id */
+  const int64_t* nbr_ptr;   /* bc_new+1 CSR offsets by prediction block id, nbr_ptr[0] = 0 */
+  const int32_t* nbr_idx;   /* training point ids in [0, n), no duplicate within a block, in the
+                               order given (the planner emits ascending (distance to centroid, id)) */
+} bv_pred_plan;
+
+/* Prediction at θ.  mean[n_new] = μ (the predicted values y*, l.12), indexed
+ * by new-point id; var[n_new] (or NULL) = diag Σ_B* (PAPER.md:242); cov (or
+ * NULL) = every block's l_b×l_b Σ_B* row-major, blocks in id order at offset
+ * Σ_{b'<b} l_b'² (l.15, "for conditional simulations").  Requires
+ * m_b + l_b ≤ 235 (the joint triangle lives in shared memory).  Errors:
+ * BV_EINVAL (invalid pred plan / θ; message names the first violation),
+ * BV_ENOTPD (Σcon of a block not positive definite; bv_last_error's
+ * failed_position = the smallest such block id).  Not collective: under
+ * multi-GPU any rank may call it alone (the point records are replicated). */
+bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp, double* mean, double* var,
+                     double* cov);
+
 /* Last error message and (after BV_ENOTPD) the smallest failing position, or
  * -1.  *msg points into the handle and is valid until the next call. */
 bv_status bv_last_error(const bv_handle* h, int32_t* failed_position, const char** msg);

@@ -82,6 +82,9 @@ def lib():
             L.or_block_nn_bruteforce.restype = C.c_int
             L.or_block_nn_bruteforce.argtypes = [C.c_int64, C.c_int, _d, C.c_int32, _i32, _i32, C.c_int32, _i64,
                                                  _i32]
+            L.or_bv_predict.restype = C.c_int
+            L.or_bv_predict.argtypes = [C.c_int64, C.c_int, _d, _d, _d, C.c_int64, _d, C.c_int32, _i32, _i64, _i32,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]
             L.or_kmeans_assign_bruteforce.restype = None
             L.or_kmeans_assign_bruteforce.argtypes = [C.c_int64, C.c_int, _d, C.c_int32, _d, _i32]
             _lib = L
@@ -225,4 +228,27 @@ def kmeans_assign_bruteforce(locs, centroids):
     cent = _c(centroids, np.float64)
     out = np.zeros(locs.shape[0], dtype=np.int32)
     lib().or_kmeans_assign_bruteforce(locs.shape[0], locs.shape[1], locs, cent.shape[0], cent, out)
+    return out
+
+
+def bv_predict(locs, y, theta, locs_new, block_new, nbr_ptr, nbr_idx, want_cov: bool = False):
+    """Alg. 2 literally → dict(mean, var[, cov (flat, per block l_b² row-major)])."""
+    locs = _c(locs, np.float64)
+    n, d = locs.shape
+    ln = _c(locs_new, np.float64)
+    bn = _c(block_new, np.int32)
+    bc = int(bn.max()) + 1 if bn.size else 0
+    mean = np.zeros(ln.shape[0])
+    var = np.zeros(ln.shape[0])
+    lsz = np.bincount(bn, minlength=bc).astype(np.int64)
+    cov = np.zeros(int(np.sum(lsz * lsz))) if want_cov else None
+    fb = C.c_int32(-1)
+    st = lib().or_bv_predict(n, d, locs, _c(y, np.float64), _c(theta, np.float64), ln.shape[0], ln, bc, bn,
+                             _c(nbr_ptr, np.int64), _c(nbr_idx, np.int32), mean.ctypes.data, var.ctypes.data,
+                             cov.ctypes.data if cov is not None else None, C.byref(fb))
+    if st:
+        raise OracleError(st, fb.value)
+    out = {"mean": mean, "var": var}
+    if cov is not None:
+        out["cov"] = cov
     return out

@@ -25,6 +25,11 @@
  *                        formulation from or_bv_loglik, so the generating-model
  *                        pin u_i ≈ ‖ε_i‖² cross-checks two formulations).
  *   or_simulate_exact    y = chol(Σθ) ε, for exact GRFs at small n.
+ *   or_bv_predict        Alg. 2 l.8-13, PAPER.md:651-662 (§S1; §2.3
+ *                        PAPER.md:194-240) taken literally per prediction block:
+ *                        Σcon, Σcross, Σlk → L = POTRF(Σcon), W = L⁻¹Σcross,
+ *                        z = L⁻¹y_NN, μ = Wᵀz, Σ_B* = Σlk − WᵀW (Σcross read as
+ *                        K(s_NN, s_B*), m×l, as in Alg. 1 — reading G8).
  *   or_block_nn_bruteforce  Alg. 1 l.7-9 mNearestNeighborsForBlock,
  *                        PAPER.md:589-591, :104 (centroid), :165 (earlier blocks
  *                        only); O(n²) brute force used to pin the planner.
@@ -384,6 +389,93 @@ int or_bv_loglik(int64_t n, int d, const double* locs, const double* y, int32_t 
                                        k_begin, k_end, nullptr, 0u);
   return bv_loglik_impl<double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads, k_begin,
                                 k_end, nullptr, perturb_seed);
+}
+
+/* Alg. 2: block-Vecchia prediction at n_new new locations.
+ *   locs (n×d) / y (n): the training data; locs_new (n_new×d); block_new
+ *   (n_new, in [0, bc_new)): the clustering g of l.4; nbr_ptr/nbr_idx (CSR by
+ *   prediction block, training ids): the NN sets of l.6 (m nearest training
+ *   points, any training point — PAPER.md:203 "from y").  Block points in
+ *   ascending new-point id (reading G13).  Outputs: mean[n_new] = μ (l.9,
+ *   l.12), var[n_new] = diag Σ_B* (PAPER.md:242), cov (may be NULL): block b's
+ *   l_b×l_b Σ_B* row-major at offset Σ_{b'<b} l_b'² (l.10-11, "for conditional
+ *   simulations", l.15).  Returns 0, 2 or 3 (non-PD; *failed_block).  FP64. */
+int or_bv_predict(int64_t n, int d, const double* locs, const double* y, const double* theta, int64_t n_new,
+                  const double* locs_new, int32_t bc_new, const int32_t* block_new, const int64_t* nbr_ptr,
+                  const int32_t* nbr_idx, double* mean, double* var, double* cov, int32_t* failed_block) {
+  if (!theta_ok(theta) || n < 1 || (d != 2 && d != 3) || n_new < 1 || bc_new < 1) return 2;
+  std::vector<int64_t> bptr((size_t)bc_new + 1, 0);
+  for (int64_t i = 0; i < n_new; ++i) {
+    if (block_new[i] < 0 || block_new[i] >= bc_new) return 2;
+    bptr[(size_t)block_new[i] + 1]++;
+  }
+  for (int32_t b = 0; b < bc_new; ++b) bptr[(size_t)b + 1] += bptr[b];
+  std::vector<int32_t> bidx((size_t)n_new);
+  {
+    std::vector<int64_t> fill(bptr.begin(), bptr.end() - 1);
+    for (int64_t i = 0; i < n_new; ++i) bidx[(size_t)fill[block_new[i]]++] = (int32_t)i;
+  }
+  std::vector<int64_t> coff((size_t)bc_new + 1, 0);
+  for (int32_t b = 0; b < bc_new; ++b) {
+    const int64_t l = bptr[(size_t)b + 1] - bptr[b];
+    coff[(size_t)b + 1] = coff[b] + l * l;
+  }
+  const double s2 = theta[0], beta = theta[1], nu = theta[2];
+  int32_t fail = -1;
+  for (int32_t b = 0; b < bc_new; ++b) {
+    const int l = (int)(bptr[(size_t)b + 1] - bptr[b]);
+    const int32_t* B = bidx.data() + bptr[b];
+    const int m = (int)(nbr_ptr[(size_t)b + 1] - nbr_ptr[b]);
+    const int32_t* NN = nbr_idx + nbr_ptr[b];
+    auto lt = [&](int32_t i) { return locs + (size_t)i * d; };
+    auto ln = [&](int32_t i) { return locs_new + (size_t)i * d; };
+    // l.8  Σlk ← cov(S_B*, S_B*)   (l×l)
+    std::vector<double> Slk((size_t)l * l);
+    for (int a = 0; a < l; ++a)
+      for (int c = 0; c < l; ++c) Slk[(size_t)a * l + c] = matern<double>(dist<double>(ln(B[a]), ln(B[c]), d), s2, beta, nu);
+    std::vector<double> mu(l, 0.0), Sb = Slk;
+    if (m > 0) {
+      // l.6  Σcon ← cov(S_NN, S_NN) (m×m);  l.7  Σcross ← cov(S_NN, S_B*) (m×l)
+      std::vector<double> Scon((size_t)m * m), W((size_t)m * l), z(m);
+      for (int a = 0; a < m; ++a)
+        for (int c = 0; c < m; ++c) Scon[(size_t)a * m + c] = matern<double>(dist<double>(lt(NN[a]), lt(NN[c]), d), s2, beta, nu);
+      for (int a = 0; a < m; ++a)
+        for (int c = 0; c < l; ++c) W[(size_t)a * l + c] = matern<double>(dist<double>(lt(NN[a]), ln(B[c]), d), s2, beta, nu);
+      for (int a = 0; a < m; ++a) z[a] = y[NN[a]];
+      // (Σcon)⁻¹ applied through its Cholesky factor: L = POTRF(Σcon), W = L⁻¹Σcross, z = L⁻¹y_NN
+      std::vector<double> L;
+      if (!potrf<double>(Scon, L, m, kPivotFloor * s2)) {
+        fail = b;
+        break;
+      }
+      for (int c = 0; c < l; ++c) trsv<double>(L, m, W.data() + c, (size_t)l);
+      trsv<double>(L, m, z.data(), 1);
+      // l.9  μ_B* = Σcrossᵀ (Σcon)⁻¹ y_NN = Wᵀz
+      for (int a = 0; a < l; ++a) {
+        double t = 0;
+        for (int q = 0; q < m; ++q) t += W[(size_t)q * l + a] * z[q];
+        mu[a] = t;
+      }
+      // l.10-11  Σ_B* = Σlk − Σcrossᵀ (Σcon)⁻¹ Σcross = Σlk − WᵀW
+      for (int a = 0; a < l; ++a)
+        for (int c = 0; c < l; ++c) {
+          double t = 0;
+          for (int q = 0; q < m; ++q) t += W[(size_t)q * l + a] * W[(size_t)q * l + c];
+          Sb[(size_t)a * l + c] = Slk[(size_t)a * l + c] - t;
+        }
+    }
+    // l.12  y_B* = μ_B*; variances = diag Σ_B*
+    for (int a = 0; a < l; ++a) {
+      mean[B[a]] = mu[a];
+      if (var) var[B[a]] = Sb[(size_t)a * l + a];
+    }
+    if (cov) std::copy(Sb.begin(), Sb.end(), cov + coff[b]);
+  }
+  if (fail >= 0) {
+    if (failed_block) *failed_block = fail;
+    return 3;
+  }
+  return 0;
 }
 
 /* Eq. (1): ℓ = −n/2 log 2π − ½ log|Σθ| − ½ yᵀΣθ⁻¹y, dense

@@ -30,7 +30,7 @@ _NAMES = {2: "BV_EINVAL", 3: "BV_ENOTPD", 4: "BV_EIO", 5: "BV_ECUDA", 6: "BV_ENC
 # every symbol include/bv.h declares (tests check the library exports them all)
 EXPORTS = ["bv_version", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_owned_range",
            "bv_loglik_host_y", "bv_last_error", "bv_launches_per_eval", "bv_stream", "bv_last_kernel_ms", "bv_destroy", "bv_partition",
-           "bv_fixed_encode", "bv_fixed_decode"]
+           "bv_fixed_encode", "bv_fixed_decode", "bv_predict"]
 
 
 class BVError(RuntimeError):
@@ -47,6 +47,11 @@ class NotPositiveDefinite(BVError):
 class _Plan(C.Structure):
     _fields_ = [("n", C.c_int64), ("d", C.c_int32), ("locs", C.c_void_p), ("y", C.c_void_p), ("bc", C.c_int32),
                 ("block_id", C.c_void_p), ("order", C.c_void_p), ("nbr_ptr", C.c_void_p), ("nbr_idx", C.c_void_p)]
+
+
+class _PredPlan(C.Structure):
+    _fields_ = [("n_new", C.c_int64), ("locs_new", C.c_void_p), ("bc_new", C.c_int32), ("block_id", C.c_void_p),
+                ("nbr_ptr", C.c_void_p), ("nbr_idx", C.c_void_p)]
 
 
 class _Dist(C.Structure):
@@ -85,7 +90,9 @@ def lib():
             L.bv_fixed_encode.argtypes = [C.c_double, C.c_void_p]
             L.bv_fixed_decode.restype = C.c_double
             L.bv_fixed_decode.argtypes = [C.c_void_p]
-            for fn in ("bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_loglik_host_y",
+            L.bv_predict.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_PredPlan), C.c_void_p, C.c_void_p,
+                                     C.c_void_p]
+            for fn in ("bv_predict", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_loglik_host_y",
                        "bv_owned_range", "bv_last_error", "bv_partition", "bv_fixed_encode"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
@@ -209,6 +216,26 @@ class BlockVecchia:
         out = C.c_double()
         self._check(self._L.bv_loglik_host_y(self._h, yp, th.ctypes.data, C.byref(out)))
         return out.value
+
+    def predict(self, theta, pred, want_cov: bool = False):
+        """Alg. 2 (bv_predict): ``pred`` has locs_new (n_new,d), block_id (n_new,) i32, nbr_ptr
+        (bc_new+1,) i64, nbr_idx (training ids) i32.  Returns (mean, var) or (mean, var, cov) with cov
+        the blocks' l_b×l_b Σ_B* row-major, concatenated in block-id order."""
+        th = self._theta(theta)
+        ln = np.ascontiguousarray(pred.locs_new, dtype=np.float64)
+        bid = np.ascontiguousarray(pred.block_id, dtype=np.int32)
+        ptr = np.ascontiguousarray(pred.nbr_ptr, dtype=np.int64)
+        idx = np.ascontiguousarray(pred.nbr_idx, dtype=np.int32)
+        nn, bc = ln.shape[0], ptr.shape[0] - 1
+        mean, var = np.zeros(nn), np.zeros(nn)
+        cov = None
+        if want_cov:
+            lsz = np.bincount(bid, minlength=bc).astype(np.int64)
+            cov = np.zeros(max(1, int(np.sum(lsz * lsz))))
+        pp = _PredPlan(nn, _ptr(ln), bc, _ptr(bid), _ptr(ptr), idx.ctypes.data if idx.size else None)
+        self._check(self._L.bv_predict(self._h, th.ctypes.data, C.byref(pp), _ptr(mean), _ptr(var),
+                                       _ptr(cov) if cov is not None else None))
+        return (mean, var, cov) if want_cov else (mean, var)
 
     @property
     def stream_ptr(self) -> int:

@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbv.so")
-SOURCES = ["bv_host.cpp", "bv_kernels.cu", "bv_block_v2.cu", "bv_block_v3.cu"]
+SOURCES = ["bv_host.cpp", "bv_kernels.cu", "bv_block_v2.cu", "bv_block_v3.cu", "bv_predict.cu"]
 HEADERS = ["bv_common.cuh", "matern.cuh", "bessel_k.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -54,6 +54,15 @@ def build(force: bool = False, verbose: bool = False, profile_phases: bool = Fal
            + ["-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}"])
     subprocess.check_call(cmd)
     os.replace(tmp, out)
+    return out
+
+
+def build_ablation(force: bool = False) -> str:
+    """libbv_fill.so: the timing ablation of SURVEY §8d (v) — Matérn fill replaced by a cheap
+    SPD fill (-DBV_ABL_FILL).  Diagnostic only; bench.py reports it as `factorization_only`."""
+    out = os.path.join(HERE, "libbv_fill.so")
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(LIB):
+        build(variant="fill", defines=["BV_ABL_FILL"])
     return out
 
 

@@ -41,6 +41,13 @@ namespace v3 {
 #ifndef BV_TRSM
 #define BV_TRSM 1
 #endif
+// Update-warp panel solves (tiles I ≥ J+2): 0 = row substitution against the
+// row-major L_JJ (DFMA; 26 FP64-pipe cycles per tile instead of the 96 of three
+// DMMA tile products), 1 = same as the chain (DMMA + refinement).  The chain's
+// own L(J+1,J) is on the critical path and keeps the short DMMA dependency chain.
+#ifndef BV_TRSM_U
+#define BV_TRSM_U BV_TRSM
+#endif
 
 constexpr int kW = 4;
 constexpr int kNT = kW * 32;
@@ -108,14 +115,21 @@ __device__ __forceinline__ void st_row_frag_rot(double* row, int rot, const doub
 }
 
 struct Layout {
-  int P, dtile, ptile, linv, lfr, misc, theta, etab, slots, tab, total_bytes;
+  int P, dtile, ptile, linv, lfr, lrow, rinv, misc, theta, etab, slots, tab, total_bytes;
   __host__ __device__ Layout(int TImax, int cap) {
     P = 0;                   // PointRec[8·TImax]
     dtile = P + 32 * TImax;  // C(J,J), row-major (chain warp only)
     ptile = dtile + 64;      // next diagonal tile's partial P(J+1,J+1) (update warps → chain)
     linv = ptile + 64;       // [2][64] L_JJ⁻¹ in DMMA fragment order (0 on padding rows)
     lfr = linv + 128;        // [2][64] L_JJ in DMMA fragment order
-    misc = lfr + 128;        // [1] chain quad, [2] fail, [3] chain warp, [4] logdet, [5..7] update-warp quads
+    lrow = lfr + 128;        // [2][64] L_JJ row-major (L_jj on the diagonal) for update-warp row solves
+#if BV_TRSM_U == 0 && BV_TRSM != 0
+    rinv = lrow + 128;       // [2][8] 1/L_jj
+    misc = rinv + 16;        // [1] chain quad, [2] fail, [3] chain warp, [4] logdet, [5..7] update-warp quads
+#else
+    rinv = lrow;  // (unused: no extra buffers unless BV_TRSM_U = 0 with a DMMA chain)
+    misc = lrow;
+#endif
     theta = misc + 8;        // Theta (≤ 20 doubles)
     etab = theta + 20;       // 2^{−j/64}, j = 0..63 (exp_neg)
     slots = etab + 64;       // cap tiles
@@ -152,14 +166,20 @@ __device__ __forceinline__ void row_solve(const double (&c)[8], const double* dl
 // 2(4i + (k&3)) + (k>>2).  Padding pivots (j ≥ N − 8J) get 1/L_jj = 0, so
 // their rows of L_JJ⁻¹ — and with them the padding columns of every
 // L(I,J) = C(I,J) L_JJ⁻ᵀ — are zero.
-__device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, int J, int m, int N, int lane,
-                                            double pfloor, double& prod, int& nbad, double& qd) {
+__device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, double* lr, double* ri, int J,
+                                            int m, int N, int lane, double pfloor, double& prod, int& nbad,
+                                            double& qd) {
   const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
   double a[8][8], rr[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int k = 0; k <= i; ++k) a[i][k] = t[8 * i + k];
+#ifdef BV_ABL_CHAIN  // timing ablation only: no pivot chain (results meaningless)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) rr[j] = a[j][j];
+  if (false)
+#endif
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     double p = a[j][j];
@@ -225,8 +245,19 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
 #pragma unroll
       for (int k = 0; k <= i; ++k) l = (k == j) ? a[i][k] : l;
       lf[o] = l;
+#if BV_TRSM_U == 0
+      lr[8 * i + j] = l;
+#endif
     }
+#if BV_TRSM_U == 0
+    double r = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r = (k == j) ? rr[k] : r;
+    ri[j] = r;
+#endif
   }
+  (void)lr;
+  (void)ri;
 #endif
 }
 
@@ -414,7 +445,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       double* li = linv + 64 * (J & 1);
       double* lj = lfr + 64 * (J & 1);
       P3_T(t0);
-      factor_tile(dtile, lj, li, J, m, N, lane, pfloor, pm, nbad, qd_in);  // a4/a7
+      factor_tile(dtile, lj, li, smem + Ly.lrow + 64 * (J & 1), smem + Ly.rinv + 8 * (J & 1), J, m, N, lane, pfloor,
+                  pm, nbad, qd_in);  // a4/a7
       int ex;
       pm = frexp(pm, &ex);
       pe += ex;
@@ -553,10 +585,15 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       P3_ADD(7, u7);
       P3_T(u8);
       {
-#if BV_TRSM == 0
+#if BV_TRSM_U == 0
         // L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2, one row per update thread (a5/a6)
+#if BV_TRSM == 0
         const double* dl = lfr + 64 * (J & 1);
         const double* ri = linv + 64 * (J & 1);
+#else
+        const double* dl = smem + Ly.lrow + 64 * (J & 1);
+        const double* ri = smem + Ly.rinv + 8 * (J & 1);
+#endif
         const int rows = (TI - J - 2) * 8;
         const int utid = (uw - 1) * 32 + lane;
 #pragma unroll 1

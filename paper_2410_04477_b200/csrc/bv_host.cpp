@@ -30,6 +30,11 @@ cudaError_t prepare_block_v1(int Nmax);
 cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                             const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
                             unsigned long long* acc, int k_begin);
+size_t predict_smem_bytes(int N);
+cudaError_t prepare_predict(size_t smem);
+cudaError_t launch_predict(int nblocks, size_t smem, cudaStream_t s, const PointRec* train, const PointRec* newp,
+                           const int32_t* nbr, const BlockDesc* desc, const Theta* th, const int64_t* cov_off,
+                           double* mean, double* var, double* cov, int32_t* status);
 cudaError_t launch_scatter_y(const double* y, const int32_t* perm_of_id, int64_t n, PointRec* pts, cudaStream_t s);
 int v2_maxt_for(int TI);
 int v3_maxt_for(int TI);
@@ -147,6 +152,7 @@ struct bv_handle {
   unsigned long long* d_acc = nullptr;
   unsigned long long* d_min = nullptr;
   int32_t* d_perm_of_id = nullptr;
+  std::vector<int32_t> h_perm_of_id;       // global id → permuted record (host copy, for bv_predict)
   double* d_y_stage = nullptr;
   int16_t* d_tabs = nullptr;
   double* d_exptab = nullptr;
@@ -566,6 +572,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   TRY(upload(h, &h->d_desc, desc.data(), desc.size()));
   TRY(upload(h, &h->d_list, list.data(), list.size()));
   TRY(upload(h, &h->d_perm_of_id, perm_of_id.data(), perm_of_id.size()));
+  h->h_perm_of_id = perm_of_id;
   TRY(upload<double>(h, &h->d_y_stage, nullptr, (size_t)n));
   TRY(upload<bv::Theta>(h, &h->d_theta, nullptr, 1));
   TRY(upload<double>(h, &h->d_u, nullptr, (size_t)h->nq));
@@ -761,3 +768,139 @@ void bv_destroy(bv_handle* h) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- prediction (Alg. 2)
+bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp, double* mean, double* var,
+                     double* cov) {
+  if (!h) return BV_EINVAL;
+  h->failed_pos = -1;
+  h->err.clear();
+  if (!theta || !pp || !mean) return fail(h, BV_EINVAL, "NULL argument");
+  if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
+  const int64_t nn = pp->n_new;
+  const int32_t bc = pp->bc_new;
+  const int d = h->d;
+  if (nn < 1 || nn > INT32_MAX) return fail(h, BV_EINVAL, "n_new must be in [1, 2^31)");
+  if (bc < 1 || (int64_t)bc > nn) return fail(h, BV_EINVAL, "bc_new must be in [1, n_new]");
+  if (!pp->locs_new || !pp->block_id || !pp->nbr_ptr) return fail(h, BV_EINVAL, "NULL pred plan array");
+  for (int64_t i = 0; i < nn * d; ++i)
+    if (!std::isfinite(pp->locs_new[i])) return fail(h, BV_EINVAL, "locs_new[" + std::to_string(i) + "] is not finite");
+  std::vector<int64_t> bptr((size_t)bc + 1, 0);
+  for (int64_t i = 0; i < nn; ++i) {
+    const int32_t b = pp->block_id[i];
+    if (b < 0 || b >= bc) return fail(h, BV_EINVAL, "block_id[" + std::to_string(i) + "] out of range");
+    bptr[(size_t)b + 1]++;
+  }
+  for (int32_t b = 0; b < bc; ++b)
+    if (bptr[(size_t)b + 1] == 0) return fail(h, BV_EINVAL, "prediction block " + std::to_string(b) + " is empty");
+  for (int32_t b = 0; b < bc; ++b) bptr[(size_t)b + 1] += bptr[b];
+  if (pp->nbr_ptr[0] != 0) return fail(h, BV_EINVAL, "nbr_ptr[0] != 0");
+  for (int32_t b = 0; b < bc; ++b)
+    if (pp->nbr_ptr[b + 1] < pp->nbr_ptr[b]) return fail(h, BV_EINVAL, "nbr_ptr decreases at " + std::to_string(b));
+  const int64_t nnz = pp->nbr_ptr[bc];
+  if (nnz > INT32_MAX) return fail(h, BV_EINVAL, "too many neighbour entries (> 2^31)");
+  if (nnz > 0 && !pp->nbr_idx) return fail(h, BV_EINVAL, "nbr_idx is NULL");
+  constexpr int kPredNmax = 235;  // predict_smem_bytes(235) ≤ 232448
+  size_t smax = 0;
+  {
+    std::vector<int32_t> stamp((size_t)h->n, -1);
+    for (int32_t b = 0; b < bc; ++b) {
+      for (int64_t q = pp->nbr_ptr[b]; q < pp->nbr_ptr[b + 1]; ++q) {
+        const int32_t id = pp->nbr_idx[q];
+        if (id < 0 || id >= h->n) return fail(h, BV_EINVAL, "nbr_idx[" + std::to_string(q) + "] out of range");
+        if (stamp[id] == b) return fail(h, BV_EINVAL, "duplicate neighbour in prediction block " + std::to_string(b));
+        stamp[id] = b;
+      }
+      const int N = (int)(pp->nbr_ptr[b + 1] - pp->nbr_ptr[b] + bptr[(size_t)b + 1] - bptr[b]);
+      if (N > kPredNmax)
+        return fail(h, BV_EINVAL, "prediction block " + std::to_string(b) + " has m+l = " + std::to_string(N) +
+                                      " > " + std::to_string(kPredNmax));
+      smax = std::max(smax, bv::predict_smem_bytes(N));
+    }
+  }
+  // block-contiguous new-point records (ascending id inside a block), descriptors, remapped neighbours
+  std::vector<bv::PointRec> np((size_t)nn);
+  std::vector<int32_t> order_new((size_t)nn);
+  {
+    std::vector<int64_t> fill(bptr.begin(), bptr.end() - 1);
+    for (int64_t i = 0; i < nn; ++i) order_new[(size_t)fill[pp->block_id[i]]++] = (int32_t)i;
+  }
+  for (int64_t p = 0; p < nn; ++p) {
+    const double* s = pp->locs_new + (size_t)order_new[p] * d;
+    np[p] = bv::PointRec{s[0], s[1], d == 3 ? s[2] : 0.0, 0.0};
+  }
+  std::vector<bv::BlockDesc> desc((size_t)bc);
+  std::vector<int64_t> coff((size_t)bc + 1, 0);
+  for (int32_t b = 0; b < bc; ++b) {
+    const int64_t l = bptr[(size_t)b + 1] - bptr[b];
+    desc[b] = bv::BlockDesc{(int32_t)bptr[b], (int32_t)l, (int32_t)(pp->nbr_ptr[b + 1] - pp->nbr_ptr[b]),
+                            (int32_t)pp->nbr_ptr[b]};
+    coff[(size_t)b + 1] = coff[b] + l * l;
+  }
+  std::vector<int32_t> nbr((size_t)std::max<int64_t>(nnz, 1), 0);
+  for (int64_t q = 0; q < nnz; ++q) nbr[(size_t)q] = h->h_perm_of_id[pp->nbr_idx[q]];
+
+  BV_CUDA(h, cudaSetDevice(h->device));
+  cudaStream_t st = h->stream;
+  bv::PointRec* d_np = nullptr;
+  int32_t *d_nbr = nullptr, *d_status = nullptr;
+  bv::BlockDesc* d_desc = nullptr;
+  int64_t* d_coff = nullptr;
+  double *d_mean = nullptr, *d_var = nullptr, *d_cov = nullptr;
+  auto release = [&]() {
+    cudaFreeAsync(d_np, st);
+    cudaFreeAsync(d_nbr, st);
+    cudaFreeAsync(d_status, st);
+    cudaFreeAsync(d_desc, st);
+    cudaFreeAsync(d_coff, st);
+    cudaFreeAsync(d_mean, st);
+    cudaFreeAsync(d_var, st);
+    cudaFreeAsync(d_cov, st);
+    cudaStreamSynchronize(st);
+  };
+#define PCALL(call)                                                                                     \
+  do {                                                                                                  \
+    cudaError_t e_ = (call);                                                                            \
+    if (e_ != cudaSuccess) {                                                                            \
+      release();                                                                                        \
+      return fail(h, e_ == cudaErrorMemoryAllocation ? BV_ENOMEM : BV_ECUDA,                            \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                                  \
+    }                                                                                                   \
+  } while (0)
+  PCALL(cudaMallocAsync((void**)&d_np, sizeof(bv::PointRec) * np.size(), st));
+  PCALL(cudaMallocAsync((void**)&d_nbr, sizeof(int32_t) * nbr.size(), st));
+  PCALL(cudaMallocAsync((void**)&d_status, sizeof(int32_t) * bc, st));
+  PCALL(cudaMallocAsync((void**)&d_desc, sizeof(bv::BlockDesc) * bc, st));
+  PCALL(cudaMallocAsync((void**)&d_coff, sizeof(int64_t) * coff.size(), st));
+  PCALL(cudaMallocAsync((void**)&d_mean, sizeof(double) * nn, st));
+  PCALL(cudaMallocAsync((void**)&d_var, sizeof(double) * nn, st));
+  if (cov) PCALL(cudaMallocAsync((void**)&d_cov, sizeof(double) * std::max<int64_t>(coff[bc], 1), st));
+  PCALL(cudaMemcpyAsync(d_np, np.data(), sizeof(bv::PointRec) * np.size(), cudaMemcpyHostToDevice, st));
+  PCALL(cudaMemcpyAsync(d_nbr, nbr.data(), sizeof(int32_t) * nbr.size(), cudaMemcpyHostToDevice, st));
+  PCALL(cudaMemcpyAsync(d_desc, desc.data(), sizeof(bv::BlockDesc) * bc, cudaMemcpyHostToDevice, st));
+  PCALL(cudaMemcpyAsync(d_coff, coff.data(), sizeof(int64_t) * coff.size(), cudaMemcpyHostToDevice, st));
+  fill_theta(*h->h_theta, theta);
+  PCALL(cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta), cudaMemcpyHostToDevice, st));
+  PCALL(bv::prepare_predict(std::max<size_t>(smax, 1024)));
+  PCALL(bv::launch_predict(bc, smax, st, h->d_pts, d_np, d_nbr, d_desc, h->d_theta, d_coff, d_mean, d_var, d_cov,
+                           d_status));
+  std::vector<double> hm((size_t)nn), hv((size_t)nn);
+  std::vector<int32_t> hs((size_t)bc);
+  PCALL(cudaMemcpyAsync(hm.data(), d_mean, sizeof(double) * nn, cudaMemcpyDeviceToHost, st));
+  PCALL(cudaMemcpyAsync(hv.data(), d_var, sizeof(double) * nn, cudaMemcpyDeviceToHost, st));
+  PCALL(cudaMemcpyAsync(hs.data(), d_status, sizeof(int32_t) * bc, cudaMemcpyDeviceToHost, st));
+  if (cov) PCALL(cudaMemcpyAsync(cov, d_cov, sizeof(double) * coff[bc], cudaMemcpyDeviceToHost, st));
+  PCALL(cudaStreamSynchronize(st));
+#undef PCALL
+  release();
+  for (int32_t b = 0; b < bc; ++b)
+    if (hs[b] != bv::kOk) {
+      h->failed_pos = b;
+      return fail(h, BV_ENOTPD, "prediction block " + std::to_string(b) + ": Sigma_con is not positive definite");
+    }
+  for (int64_t p = 0; p < nn; ++p) {
+    mean[order_new[p]] = hm[p];
+    if (var) var[order_new[p]] = hv[p];
+  }
+  return BV_OK;
+}

@@ -97,6 +97,35 @@ def test_c4_full_size_sampled_parity():
     bv.close()
 
 
+def test_c5_shaped_m200_sampled_parity():
+    """c5's block-size mix at m = 200 (joint sizes to ~263, beyond the 240 a packed triangle fits;
+    the left-looking slot layout runs them one CTA per SM) at n = 200k: whole ℓ vs the FP64 oracle
+    and element-wise terms on the largest-N positions and the head.  y is simulated once with the
+    nested m = 60 plan (c5 y generated with m_sim = 60)."""
+    theta = (1.0, 0.078809, 0.5)
+    kw = dict(n=200_000, bc=10_000, cfg=5)
+    p60 = bvgen.make_plan("c5", m=60, **kw)
+    y = oracle.simulate_bv(p60, theta, bvgen.normal(502, p60.n))
+    p = bvgen.make_plan("c5", m=200, **kw).with_y(y)
+    l, mk = p.block_sizes()
+    N = l + mk
+    assert N.max() > 240
+    bv = BlockVecchia(p)
+    ll, d, u = bv.loglik_terms(theta)
+    o64 = oracle.bv_loglik(p, theta, per_block=True)
+    rel = abs(ll - o64["loglik"]) / abs(o64["loglik"])
+    assert rel <= 1e-9, rel
+    big = np.sort(np.argsort(-N, kind="stable")[:300])
+    for idx, lab in ((big, "largest N"), (np.arange(300), "head")):
+        dd, uu = d[idx], u[idx]
+        od, ou = o64["d"][idx], o64["u"][idx]
+        sc = np.abs(ou) + np.abs(od) + l[idx] * 1.8378770664093456
+        e = max(np.max(np.abs(dd - od) / sc), np.max(np.abs(uu - ou) / sc))
+        print("c5 m=200", lab, "max term err", e, "ll rel", rel)
+        assert e <= 1e-10, (lab, e)  # ν = 0.5: κ ≤ 3e6, strict bar everywhere (SURVEY P2/P11)
+    bv.close()
+
+
 # ---------------------------------------------------------------- edge cases
 @pytest.mark.parametrize("n,bc,m,d", [
     (50, 1, 10, 2),        # one block, no neighbours (m_1 = 0, PAPER.md:583)
@@ -105,13 +134,11 @@ def test_c4_full_size_sampled_parity():
     (333, 17, 45, 3),      # ragged 3D
     (700, 7, 100, 2),      # large blocks (N ≈ 200)
     (64, 2, 70, 2),        # second block conditions on all of the first (m > l_1)
+    (600, 6, 180, 2),      # joint sizes up to ~280 (c5 at m = 200 reaches 263): one CTA per SM
 ])
 def test_edge_shapes_parity(n, bc, m, d):
     theta = (1.2, 0.09, 1.5)
     p = bvgen.make_plan("c4" if d == 3 else "c1", n=n, bc=bc, m=m, d=d, cfg=31)
-    l, mk = p.block_sizes()
-    if (l + mk).max() > 224:
-        pytest.skip("joint size beyond this build's shared-memory limit")
     p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(3102, n)))
     full_parity(p, theta, f"edge n={n} bc={bc} m={m} d={d}")
 
@@ -192,3 +219,14 @@ def test_generating_model_on_gpu():
     _, d, u = BlockVecchia(p).loglik_terms(theta)
     e2 = np.array([np.sum(eps[np.where(p.block_id == b)[0]] ** 2) for b in p.order])
     assert np.max(np.abs(u - e2) / e2) <= 1e-11
+
+
+def test_joint_size_beyond_limit_rejected():
+    """N = m + l above the largest joint size the shared-memory layout holds (295) → BV_EINVAL naming
+    the first offending position, never a silent fallback."""
+    p = bvgen.make_plan("c1", n=1200, bc=3, m=300, cfg=33)
+    l, mk = p.block_sizes()
+    assert (l + mk).max() > 295
+    with pytest.raises(BVError) as ei:
+        BlockVecchia(p, device=0)
+    assert ei.value.status == 2 and "largest joint size" in str(ei.value)

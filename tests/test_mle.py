@@ -1,0 +1,77 @@
+"""The c2 MLE harness (paper_2410_04477_b200/mle.py): a bounded derivative-free maximisation of
+ℓ(θ) over (σ², β, ν).  CPU: the driver, run on the oracle's ℓ, reaches a local
+maximum that beats the generating θ.  GPU: the driver on the library's ℓ follows the same path
+as on the oracle's (ℓ agrees to ~1e-13, so the proposals coincide) and lands on the same θ̂."""
+import math
+
+import numpy as np
+import pytest
+
+import bvgen
+import oracle
+from paper_2410_04477_b200.mle import fit
+
+THETA_TRUE = (1.0, 0.1, 1.5)
+
+
+def small_plan(n=400, bc=20, m=20):
+    p = bvgen.make_plan("c2", n=n, bc=bc, m=m, cfg=61)
+    return p.with_y(oracle.simulate_bv(p, THETA_TRUE, bvgen.normal(6102, p.n)))
+
+
+def oracle_ll(p):
+    return lambda th: oracle.bv_loglik(p, th, per_block=False)["loglik"]
+
+
+def test_mle_on_oracle_is_a_local_maximum():
+    p = small_plan()
+    ll = oracle_ll(p)
+    r = fit(ll, max_evals=400)
+    th = r["theta"]
+    assert r["n_evals"] <= 400 and math.isfinite(r["loglik"])
+    assert r["loglik"] >= ll(THETA_TRUE) - 1e-9  # the maximiser beats the truth
+    for i in range(3):  # no coordinate move of ±1% improves it beyond the stopping tolerance
+        for f in (0.99, 1.01):
+            t2 = list(th)
+            t2[i] *= f
+            assert ll(tuple(t2)) <= r["loglik"] + 1e-6 * abs(r["loglik"])
+    # the estimate is in the neighbourhood of the generating θ (n = 400: loose)
+    assert 0.2 < th[0] < 5 and 0.02 < th[1] < 0.5 and 0.3 < th[2] < 3
+
+
+def test_mle_not_pd_scores_minus_inf():
+    """A status-coded failure (the library's NOT_PD) scores −∞ and the search carries on;
+    any other exception propagates."""
+    calls = []
+
+    class E(RuntimeError):
+        status = 3
+
+    def ll(th):
+        calls.append(th)
+        if len(calls) % 7 == 1:  # every 7th proposal, starting with the first, is "not PD"
+            raise E("not PD")
+        return -((math.log(th[0])) ** 2 + (math.log(th[1] / 0.05)) ** 2 + (th[2] - 1.2) ** 2)
+
+    r = fit(ll, max_evals=600)
+    assert abs(r["theta"][1] - 0.05) < 1e-3 and abs(r["theta"][2] - 1.2) < 1e-3
+    assert r["trace"][0][1] == -math.inf and math.isfinite(r["loglik"])
+
+    def bad(th):
+        raise KeyError("a bug, not a status")
+
+    with pytest.raises(KeyError):
+        fit(bad, max_evals=10)
+
+
+@pytest.mark.gpu
+def test_mle_gpu_matches_oracle_path():
+    from paper_2410_04477_b200 import BlockVecchia
+    p = small_plan(n=2000, bc=50, m=30)
+    bv = BlockVecchia(p)
+    rg = fit(bv.loglik, max_evals=300)
+    ro = fit(oracle_ll(p), max_evals=300)
+    bv.close()
+    print("gpu", rg["theta"], rg["loglik"], rg["n_evals"], "oracle", ro["theta"], ro["loglik"], ro["n_evals"])
+    assert abs(rg["loglik"] - ro["loglik"]) <= 1e-9 * abs(ro["loglik"])
+    np.testing.assert_allclose(rg["theta"], ro["theta"], rtol=1e-5)
