@@ -41,6 +41,18 @@ namespace v3 {
 #ifndef BV_TRSM
 #define BV_TRSM 1
 #endif
+// Refinement of the DMMA panel solve only where L_JJ is ill-conditioned: the
+// explicit-inverse product C L_JJ⁻ᵀ has relative error ~ u·κ(L_JJ), which for a
+// tile whose pivots L_jj spread by less than BV_REF_RATIO (a lower bound on
+// κ(L_JJ) that the Cholesky pivots of a nearly singular tile expose) is at the
+// level of substitution; above it the FP64 refinement step runs.  The flag is
+// per CTA and panel (uniform: no divergence).  0 = always refine.
+// Measured at c4 (gpurun_out/ab5, round 1): always refining 199 evals/s; ratio
+// 16: 188; never: 193 (and fails c3 parity) — the panel solves are not on the
+// kernel's critical resource, so the default keeps the refinement everywhere.
+#ifndef BV_REF_RATIO
+#define BV_REF_RATIO 0
+#endif
 // Update-warp panel solves (tiles I ≥ J+2): 0 = row substitution against the
 // row-major L_JJ (DFMA; 26 FP64-pipe cycles per tile instead of the 96 of three
 // DMMA tile products), 1 = same as the chain (DMMA + refinement).  The chain's
@@ -49,7 +61,13 @@ namespace v3 {
 #define BV_TRSM_U BV_TRSM
 #endif
 
-constexpr int kW = 4;
+// Measured at c4 (gpurun_out/ab7): kW = 4 (5 CTAs/SM) 197 evals/s, 5 → 187,
+// 6 → 180, 8 (2 CTAs/SM) → 166.  Resident CTAs vs throughput at kW = 4
+// (ab6, shared memory padded): 1/2/3/4/5 CTAs per SM → 73/127/164/187/199.
+#ifndef BV_KW
+#define BV_KW 4
+#endif
+constexpr int kW = BV_KW;  // warps per CTA: 1 chain warp + kW−1 update warps
 constexpr int kNT = kW * 32;
 constexpr int kBarG = 1, kBarF = 2, kBarE = 3, kBarU = 4, kBarH = 5;  // named barriers (0 = __syncthreads)
 
@@ -130,7 +148,7 @@ struct Layout {
     rinv = lrow;  // (unused: no extra buffers unless BV_TRSM_U = 0 with a DMMA chain)
     misc = lrow;
 #endif
-    theta = misc + 8;        // Theta (≤ 20 doubles)
+    theta = misc + ((kW + 7) & ~1);  // Theta (≤ 20 doubles); misc[4+kW+(J&1)] = refine flag of panel J
     etab = theta + 20;       // 2^{−j/64}, j = 0..63 (exp_neg)
     slots = etab + 64;       // cap tiles
     tab = slots + 64 * cap;  // int16 slot table (TImax²)
@@ -168,9 +186,10 @@ __device__ __forceinline__ void row_solve(const double (&c)[8], const double* dl
 // L(I,J) = C(I,J) L_JJ⁻ᵀ — are zero.
 __device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, double* lr, double* ri, int J,
                                             int m, int N, int lane, double pfloor, double& prod, int& nbad,
-                                            double& qd) {
+                                            double& qd, double& spread) {
   const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
   double a[8][8], rr[8];
+  double pmax = 0.0, pmin = 1.7976931348623157e308;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -193,6 +212,10 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
     const double lv = p * r;
     rr[j] = rv;
     a[j][j] = lv;
+    if (real) {
+      pmax = fmax(pmax, p);
+      pmin = fmin(pmin, p);
+    }
 #pragma unroll
     for (int i = j + 1; i < 8; ++i) {
       const double x = a[i][j] * rv;
@@ -203,6 +226,7 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
 #pragma unroll
       for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
   }
+  spread = pmax / pmin;  // (max L_jj / min L_jj)²
 #pragma unroll
   for (int i = 1; i < 8; ++i)
     if (i == yr) {
@@ -270,7 +294,7 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
 // Returns the lane's two results (row g, columns 2t, 2t+1) for the y-row term.
 template <int NT>
 __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 bi, double2 bl, int g, int t,
-                                            double2 (&out)[NT]) {
+                                            double2 (&out)[NT], bool refine = true) {
   double x0[NT], x1[NT], cc0[NT], cc1[NT];
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
@@ -285,6 +309,7 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
   }
   __syncwarp();
 #if BV_TRSM == 1
+  if (refine) {
 #pragma unroll
   for (int i = 0; i < NT; ++i) sts2(tile[i] + 8 * g + 2 * t, x0[i], x1[i]);
   __syncwarp();
@@ -305,6 +330,7 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     dmma884(x0[i], x1[i], ra[4], bi.y);
   }
   __syncwarp();
+  }
 #else
   (void)bl;
   (void)cc0;
@@ -317,10 +343,10 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     out[i] = make_double2(x0[i], x1[i]);
   }
 }
-__device__ __forceinline__ double2 tile_trsm(double* tile, double2 bi, double2 bl, int g, int t) {
+__device__ __forceinline__ double2 tile_trsm(double* tile, double2 bi, double2 bl, int g, int t, bool refine = true) {
   double* const tl[1] = {tile};
   double2 o[1];
-  tile_trsm_n<1>(tl, bi, bl, g, t, o);
+  tile_trsm_n<1>(tl, bi, bl, g, t, o, refine);
   return o[0];
 }
 
@@ -365,7 +391,7 @@ constexpr int kV3GenUnroll = BV_V3_GEN_UNROLL;  // half-tiles in flight per upda
 #ifndef BV_MINB_SMALL
 #define BV_MINB_SMALL 5
 #endif
-constexpr int v3_minb(int maxt) { return maxt <= 5 ? BV_MINB_SMALL : 4; }
+constexpr int v3_minb(int maxt) { return kW == 4 ? (maxt <= 5 ? BV_MINB_SMALL : 4) : (kW <= 6 ? 3 : 2); }
 
 template <int MAXT, int KIND>
 __global__ void __launch_bounds__(kNT, v3_minb(MAXT))
@@ -434,7 +460,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   }
   __syncthreads();
   const int cw = (int)misc[3];
-  const int uw = (warp - cw) & (kW - 1);  // 0 = chain warp, 1..3 = update warps
+  const int uw = (warp - cw + kW) % kW;  // 0 = chain warp, 1..kW−1 = update warps
   const double pfloor = kPivotFloor * th.sigma2;
 
   if (uw == 0) {
@@ -445,8 +471,16 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       double* li = linv + 64 * (J & 1);
       double* lj = lfr + 64 * (J & 1);
       P3_T(t0);
+      double spread;
       factor_tile(dtile, lj, li, smem + Ly.lrow + 64 * (J & 1), smem + Ly.rinv + 8 * (J & 1), J, m, N, lane, pfloor,
-                  pm, nbad, qd_in);  // a4/a7
+                  pm, nbad, qd_in, spread);  // a4/a7
+#if BV_REF_RATIO > 0
+      const bool refine = !(spread <= (double)BV_REF_RATIO * (double)BV_REF_RATIO);
+      if (lane == 0) misc[4 + kW + (J & 1)] = refine ? 1.0 : 0.0;
+#else
+      constexpr bool refine = true;
+      (void)spread;
+#endif
       int ex;
       pm = frexp(pm, &ex);
       pe += ex;
@@ -478,7 +512,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
               if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
           }
 #else
-          const double2 d = tile_trsm(slots + 64 * tab[TJ * TI + J], bi, bl, g, t);
+          const double2 d = tile_trsm(slots + 64 * tab[TJ * TI + J], bi, bl, g, t, refine);
           if (g == (N & 7)) qd_t += yrow_sq(d, J, t, m, N);
 #endif
         }
@@ -501,7 +535,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         __syncwarp();
         if (lane < 8) st_row_frag_rot(row, (lane & 7) >> 1, x);
 #else
-        const double2 d = tile_trsm(tj, bi, bl, g, t);
+        const double2 d = tile_trsm(tj, bi, bl, g, t, refine);
         if (8 * (J + 1) + g == N) qd_t += yrow_sq(d, J, t, m, N);  // the y row: u += Σ_{j≥m} z_j²
 #endif
       }
@@ -571,7 +605,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
 #undef BV_NS
           default: break;
         }
-        bar_sync(kBarU, 96);  // ptile generated by all update threads
+        bar_sync(kBarU, (kW - 1) * 32);  // ptile generated by all update threads
         if (uw == 1) {        // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp
           double* pp = ptile + 8 * g + 2 * t;
           const double2 av = lds2(pp);
@@ -597,7 +631,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         const int rows = (TI - J - 2) * 8;
         const int utid = (uw - 1) * 32 + lane;
 #pragma unroll 1
-        for (int rr = utid; rr < rows; rr += 96) {
+        for (int rr = utid; rr < rows; rr += (kW - 1) * 32) {
           const int I = J + 2 + (rr >> 3), gg = rr & 7;
           double* row = slots + 64 * tab[I * TI + J] + 8 * gg;
           double c[8], x[8];
@@ -614,6 +648,11 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         // L(I,J) = C(I,J) L_JJ⁻ᵀ for this warp's tiles I = J+u+3s > J+1 (a5/a6)
         const double2 bi = lds2(linv + 64 * (J & 1) + 2 * lane);
         const double2 bl = lds2(lfr + 64 * (J & 1) + 2 * lane);
+#if BV_REF_RATIO > 0
+        const bool refine = misc[4 + kW + (J & 1)] != 0.0;
+#else
+        constexpr bool refine = true;
+#endif
         // two tiles in flight: their DMMA / shared-memory round trips interleave
 #pragma unroll 1
         for (int I = J + uw + (uw == 1 ? kW - 1 : 0); I < TI; I += 2 * (kW - 1)) {
@@ -621,11 +660,11 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           if (I2 < TI) {
             double* const tl[2] = {slots + 64 * tab[I * TI + J], slots + 64 * tab[I2 * TI + J]};
             double2 d[2];
-            tile_trsm_n<2>(tl, bi, bl, g, t, d);
+            tile_trsm_n<2>(tl, bi, bl, g, t, d, refine);
             if (8 * I + g == N) qd_u += yrow_sq(d[0], J, t, m, N);  // the y row (a8)
             if (8 * I2 + g == N) qd_u += yrow_sq(d[1], J, t, m, N);
           } else {
-            const double2 d = tile_trsm(slots + 64 * tab[I * TI + J], bi, bl, g, t);
+            const double2 d = tile_trsm(slots + 64 * tab[I * TI + J], bi, bl, g, t, refine);
             if (8 * I + g == N) qd_u += yrow_sq(d, J, t, m, N);
           }
         }
@@ -670,7 +709,9 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     int st = fail ? kNotPD : kOk;
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     const double logdet = fail ? 0.0 : misc[4];
-    const double quad = fail ? 0.0 : ((misc[1] + misc[5]) + misc[6]) + misc[7];
+    double quad = misc[1];
+    for (int w = 1; w < kW; ++w) quad += misc[4 + w];  // fixed order: bitwise reproducible
+    quad = fail ? 0.0 : quad;
     if (!fail) {
       const double tk = -0.5 * (quad + logdet + (double)l * kLn2Pi);
       if (fixed_encode(tk, c)) st = kTermRange;
@@ -707,7 +748,17 @@ int v3_maxt_for(int TI) {
   return -1;
 }
 
-size_t v3_smem_bytes(int TImax, int cap) { return (size_t)v3::Layout(TImax, cap).total_bytes; }
+#ifndef BV_MIN_SMEM  // A/B only: pad the dynamic shared memory to cap resident CTAs per SM
+#define BV_MIN_SMEM 0
+#endif
+size_t v3_smem_bytes(int TImax, int cap) {
+  const size_t b = (size_t)v3::Layout(TImax, cap).total_bytes;
+#if BV_MIN_SMEM > 0
+  return b < (size_t)BV_MIN_SMEM ? (size_t)BV_MIN_SMEM : b;
+#else
+  return b;
+#endif
+}
 
 template <int MAXT>
 static cudaError_t v3_prep(size_t smem) {

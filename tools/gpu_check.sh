@@ -7,7 +7,8 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>
 python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests exit $?" >> $O/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke exit $?" >> $O/smoke.log
-timeout 600 python bench.py --config $cfg > $O/bench.log 2>&1; echo "bench exit $?" >> $O/bench.log
+timeout 900 python bench.py --config $cfg > $O/bench.log 2>&1; echo "bench exit $?" >> $O/bench.log
+timeout 600 python bench.py --impl reference --config $cfg --steps 3 --warmup 1 > $O/bench_ref.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
    python tools/prof_run.py $cfg 2 > $O/ncu_launch.log 2>&1
 skip=$(python - <<PY
