@@ -391,7 +391,14 @@ constexpr int kV3GenUnroll = BV_V3_GEN_UNROLL;  // half-tiles in flight per upda
 #ifndef BV_MINB_SMALL
 #define BV_MINB_SMALL 5
 #endif
-constexpr int v3_minb(int maxt) { return kW == 4 ? (maxt <= 5 ? BV_MINB_SMALL : 4) : (kW <= 6 ? 3 : 2); }
+// MAXT ≤ 2 (TI ≤ 7, N ≤ 55: c5 at m = 30): shared memory admits far more CTAs,
+// but 6 or 8 per SM (spilling) measured the same 400 evals/s at c5 m = 30 (ab8).
+#ifndef BV_MINB_TINY
+#define BV_MINB_TINY 5
+#endif
+constexpr int v3_minb(int maxt) {
+  return kW == 4 ? (maxt <= 2 ? BV_MINB_TINY : maxt <= 5 ? BV_MINB_SMALL : 4) : (kW <= 6 ? 3 : 2);
+}
 
 template <int MAXT, int KIND>
 __global__ void __launch_bounds__(kNT, v3_minb(MAXT))
