@@ -30,6 +30,9 @@ cudaError_t prepare_block_v1(int Nmax);
 cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                             const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
                             unsigned long long* acc, int k_begin);
+cudaError_t launch_cv(int kind, int count, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
+                      const BlockDesc* desc, const int32_t* list, const Theta* th, const double* etab, double* u,
+                      double* d, unsigned long long* acc, int k_begin);
 size_t predict_smem_bytes(int N);
 cudaError_t prepare_predict(size_t smem);
 cudaError_t launch_predict(int nblocks, size_t smem, cudaStream_t s, const PointRec* train, const PointRec* newp,
@@ -538,7 +541,14 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   std::vector<int32_t> list((size_t)h->nq);
   for (int32_t q = 0; q < h->nq; ++q) list[q] = q;
   auto Nq = [&](int32_t q) { return desc[q].l + desc[q].m; };
-  auto bkey = [&](int32_t q) { return use_v1 ? (Nq(q) + kBucketWidth - 1) / kBucketWidth : (Nq(q) + 8) >> 3; };
+  // classic-Vecchia positions (block size 1, m ≤ 31: joint size ≤ 32) go to the warp-per-position
+  // kernel (bv_cv.cu) as bucket key 0 (launched last); BV_NO_CV=1 keeps them in the block kernel
+  const char* nocv = std::getenv("BV_NO_CV");
+  const bool cv_ok = !use_v1 && !use_v2 && !(nocv && nocv[0] == '1');
+  auto is_cv = [&](int32_t q) { return cv_ok && desc[q].l == 1 && desc[q].m <= 31; };
+  auto bkey = [&](int32_t q) {
+    return use_v1 ? (Nq(q) + kBucketWidth - 1) / kBucketWidth : is_cv(q) ? 0 : (Nq(q) + 8) >> 3;
+  };
   std::stable_sort(list.begin(), list.end(), [&](int32_t a, int32_t b) {
     if (bkey(a) != bkey(b)) return bkey(a) > bkey(b);
     if (Nq(a) != Nq(b)) return Nq(a) > Nq(b);
@@ -558,6 +568,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
       const int Nb = std::min(Nlimit, bkey(list[i]) * kBucketWidth);
       h->buckets.push_back(Bucket{Nb, j - i, i, 0});
       maxN = std::max(maxN, Nb);
+    } else if (bkey(list[i]) == 0) {
+      h->buckets.push_back(Bucket{0, j - i, i, 0});  // classic-Vecchia warp kernel
     } else {
       const int TI = bkey(list[i]);
       h->buckets.push_back(Bucket{TI, j - i, i, slot_tables.cap[TI]});
@@ -635,6 +647,9 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
         e = bv::launch_block_v2(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
                                 h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
                                 h->d_d, h->d_acc, h->kb);
+      else if (b.Nmax == 0)
+        e = bv::launch_cv(kind, b.count, st, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset, h->d_theta,
+                          h->d_exptab, h->d_u, h->d_d, h->d_acc, h->kb);
       else
         e = bv::launch_block_v3(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
                                 h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,

@@ -230,3 +230,40 @@ def test_joint_size_beyond_limit_rejected():
     with pytest.raises(BVError) as ei:
         BlockVecchia(p, device=0)
     assert ei.value.status == 2 and "largest joint size" in str(ei.value)
+
+
+# ------------------------------------------------------- classic Vecchia
+@pytest.mark.parametrize("theta,m", [((1.0, 0.078809, 0.5), 30), ((1.0, 0.052537, 1.5), 20),
+                                     ((0.9, 0.06, 1.31), 31), ((1.2, 0.1, 2.5), 8)])
+def test_classic_vecchia_warp_kernel_parity(theta, m):
+    """bc = n (block size 1) runs the warp-per-position kernel (bv_cv.cu): terms and ℓ
+    vs the FP64/80-bit oracle (Alg. 1 literal), and ℓ vs the textbook classic-Vecchia oracle."""
+    n = 1500
+    p = bvgen.make_plan("c1", n=n, bc=n, m=m, cfg=37)
+    p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(3702, n)))
+    s = full_parity(p, theta, f"cv m={m} {theta}")
+    pt = np.empty(n, dtype=np.int32)  # singleton block b holds point pt[b]
+    pt[p.block_id] = np.arange(n, dtype=np.int32)
+    point_order = pt[p.order]
+    cv = oracle.classic_vecchia(p.locs, p.y, point_order, p.nbr_ptr, p.nbr_idx, theta)
+    bv = BlockVecchia(p)
+    ll = bv.loglik(theta)
+    bv.close()
+    assert abs(ll - cv) <= 1e-9 * abs(cv), (ll, cv)
+
+
+def test_classic_vecchia_kernel_equals_block_kernel(monkeypatch):
+    """The same bc = n plan through the warp kernel and (BV_NO_CV=1) through the block kernel."""
+    theta = (1.0, 0.078809, 1.5)
+    p = bvgen.make_plan("c1", n=800, bc=800, m=25, cfg=38)
+    p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(3802, 800)))
+    a = BlockVecchia(p)
+    la, da, ua = a.loglik_terms(theta)
+    a.close()
+    monkeypatch.setenv("BV_NO_CV", "1")
+    b = BlockVecchia(p)
+    lb, db, ub = b.loglik_terms(theta)
+    b.close()
+    sc = np.abs(ua) + np.abs(da) + 1.8378770664093456
+    assert np.max(np.abs(da - db) / sc) <= 1e-12 and np.max(np.abs(ua - ub) / sc) <= 1e-12
+    assert abs(la - lb) <= 1e-12 * abs(la)
