@@ -149,6 +149,36 @@ typedef struct {
 bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp, double* mean, double* var,
                      double* cov);
 
+/* ---- GPU plan construction (Alg. 1 l.4-9) ----
+ * The preprocessing the paper runs once per fit and excludes from timing
+ * (PAPER.md:411).  Exact selections with total orders, so the results are
+ * bit-identical to any exact implementation (tests: the CPU planner in
+ * bvgen/).  Host pointers in and out; device = CUDA ordinal.  Not collective. */
+
+/* Lloyd K-means (Alg. 1 l.5).  locs n*d row-major; init_idx:
+ * k distinct point ids, the initial centroids (drawn by the caller's seeded
+ * RNG).  Each iteration: every point to the nearest centroid (squared distance
+ * summed in x, y, z order, no FMA contraction; ties → lower id); empty
+ * clusters (ascending id) take the farthest point of a cluster with ≥ 2
+ * members (ties → lowest id); centroids = member means summed in ascending
+ * point id.  Stops when the assignment repeats or after max_iter iterations.
+ * Outputs assign[n], cent[k*d], *iters (may be NULL).  BV_EINVAL on bad
+ * arguments (1 ≤ k ≤ n < 2^31, d ∈ {2,3}). */
+bv_status bv_plan_kmeans(int32_t device, int64_t n, int32_t d, const double* locs, int32_t k, const int32_t* init_idx,
+                         int32_t max_iter, int32_t* assign, double* cent, int32_t* iters);
+
+/* mNearestNeighborsForBlock (Alg. 1 l.7-9): for every position k of the order
+ * ζ (order[k] = block id), the m_k = min(m, #points in earlier blocks) points
+ * of blocks at positions < k nearest the block centroid (mean of
+ * its points), ascending (d², id).  nbr_ptr[bc+1] is written
+ * (CSR by position); nbr_idx needs room for nbr_ptr[bc] ≤ bc*m ids.  m ≤ 256.
+ * BV_EINVAL: bad block ids / order / empty block / m. */
+bv_status bv_plan_block_nn(int32_t device, int64_t n, int32_t d, const double* locs, int32_t bc, const int32_t* block_id,
+                           const int32_t* order, int32_t m, int64_t* nbr_ptr, int32_t* nbr_idx);
+
+/* Message of the last failed bv_plan_* call on this thread ("" after success). */
+const char* bv_plan_last_error(void);
+
 /* Last error message and (after BV_ENOTPD) the smallest failing position, or
  * -1.  *msg points into the handle and is valid until the next call. */
 bv_status bv_last_error(const bv_handle* h, int32_t* failed_position, const char** msg);

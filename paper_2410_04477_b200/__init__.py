@@ -18,7 +18,7 @@ import threading
 
 import numpy as np
 
-__all__ = ["BlockVecchia", "BVError", "NotPositiveDefinite", "lib", "nccl_unique_id", "partition",
+__all__ = ["BlockVecchia", "BVError", "gpu_kmeans", "gpu_block_nn", "NotPositiveDefinite", "lib", "nccl_unique_id", "partition",
            "fixed_encode", "fixed_decode", "LIB_PATH"]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -30,7 +30,8 @@ _NAMES = {2: "BV_EINVAL", 3: "BV_ENOTPD", 4: "BV_EIO", 5: "BV_ECUDA", 6: "BV_ENC
 # every symbol include/bv.h declares (tests check the library exports them all)
 EXPORTS = ["bv_version", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_owned_range",
            "bv_loglik_host_y", "bv_last_error", "bv_launches_per_eval", "bv_stream", "bv_last_kernel_ms", "bv_destroy", "bv_partition",
-           "bv_fixed_encode", "bv_fixed_decode", "bv_predict"]
+           "bv_fixed_encode", "bv_fixed_decode", "bv_predict", "bv_plan_kmeans", "bv_plan_block_nn",
+           "bv_plan_last_error"]
 
 
 class BVError(RuntimeError):
@@ -92,7 +93,12 @@ def lib():
             L.bv_fixed_decode.argtypes = [C.c_void_p]
             L.bv_predict.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(_PredPlan), C.c_void_p, C.c_void_p,
                                      C.c_void_p]
-            for fn in ("bv_predict", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_loglik_host_y",
+            L.bv_plan_kmeans.argtypes = [C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                         C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(C.c_int32)]
+            L.bv_plan_block_nn.argtypes = [C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                           C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+            L.bv_plan_last_error.restype = C.c_char_p
+            for fn in ("bv_plan_kmeans", "bv_plan_block_nn", "bv_predict", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_loglik_host_y",
                        "bv_owned_range", "bv_last_error", "bv_partition", "bv_fixed_encode"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
@@ -133,6 +139,41 @@ def fixed_encode(t: float) -> np.ndarray:
 def fixed_decode(acc) -> float:
     a = np.ascontiguousarray(acc, dtype=np.uint64)
     return lib().bv_fixed_decode(a.ctypes.data)
+
+
+def _plan_check(st):
+    if st != BV_OK:
+        raise BVError(st, (lib().bv_plan_last_error() or b"").decode())
+
+
+def gpu_kmeans(locs, bc: int, init_idx, max_iter: int = 100, device: int = 0):
+    """Lloyd K-means on the GPU (bv_plan_kmeans; Alg. 1 l.5) →
+    (assign, centroids, iterations); bit-identical to the CPU planner for the same init_idx."""
+    L = lib()
+    locs = np.ascontiguousarray(locs, dtype=np.float64)
+    n, d = locs.shape
+    init = np.ascontiguousarray(init_idx, dtype=np.int32)
+    assign = np.zeros(n, dtype=np.int32)
+    cent = np.zeros((bc, d))
+    it = C.c_int32(0)
+    _plan_check(L.bv_plan_kmeans(device, n, d, _ptr(locs), int(bc), _ptr(init), int(max_iter), _ptr(assign),
+                                 _ptr(cent), C.byref(it)))
+    return assign, cent, it.value
+
+
+def gpu_block_nn(locs, block_id, order, m: int, device: int = 0):
+    """mNearestNeighborsForBlock on the GPU (bv_plan_block_nn; Alg. 1 l.7-9) → (nbr_ptr, nbr_idx)."""
+    L = lib()
+    locs = np.ascontiguousarray(locs, dtype=np.float64)
+    n, d = locs.shape
+    bid = np.ascontiguousarray(block_id, dtype=np.int32)
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    bc = order.shape[0]
+    ptr = np.zeros(bc + 1, dtype=np.int64)
+    idx = np.zeros(max(1, bc * int(m)), dtype=np.int32)
+    _plan_check(L.bv_plan_block_nn(device, n, d, _ptr(locs), bc, _ptr(bid), _ptr(order), int(m), _ptr(ptr),
+                                   _ptr(idx)))
+    return ptr, idx[: ptr[-1]].copy()
 
 
 class BlockVecchia:

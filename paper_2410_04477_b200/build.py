@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbv.so")
-SOURCES = ["bv_host.cpp", "bv_kernels.cu", "bv_block_v2.cu", "bv_block_v3.cu", "bv_predict.cu", "bv_cv.cu"]
+SOURCES = ["bv_host.cpp", "bv_kernels.cu", "bv_block_v2.cu", "bv_block_v3.cu", "bv_predict.cu", "bv_cv.cu", "bv_plan.cu"]
 HEADERS = ["bv_common.cuh", "matern.cuh", "bessel_k.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
