@@ -219,7 +219,11 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
 #pragma unroll
     for (int i = j + 1; i < 8; ++i) {
       const double x = a[i][j] * rv;
+#ifdef BV_CHAIN_NOCORR  // A/B only: drop the correction step (fewer chain instructions, less accurate)
+      a[i][j] = x;
+#else
       a[i][j] = fma(fma(-x, lv, a[i][j]), rv, x);
+#endif
     }
 #pragma unroll
     for (int i = j + 1; i < 8; ++i)

@@ -19,7 +19,14 @@ struct alignas(16) Theta {
   int32_t kind;     // MaternKind; closed forms iff ν ∈ {0.5, 1.5, 2.5} exactly
   int32_t pad0;
   double gen[10];   // ν-only constants of the general-ν K_ν evaluator (host-computed)
+  const double* nutab;  // device address of the ν-only node/coefficient table (bessel_k.cuh)
 };
+// The θ buffer on the device (and its pinned host twin) is kThetaSlots Theta-sized
+// slots: slot 0 = Theta, slots 1.. = the kNuTab doubles of the general-ν table.
+constexpr int kNuTrapNodes = 28;   // trapezoid nodes t_k = k·h, k = 1..28, h = 0.15 (2 < x ≤ 22)
+constexpr int kNuAsymTerms = 20;   // asymptotic-series coefficients (x > 22)
+constexpr int kNuTab = 2 * kNuTrapNodes + kNuAsymTerms;
+constexpr int kThetaSlots = 1 + (kNuTab * 8 + (int)sizeof(double) * 16 - 1) / ((int)sizeof(double) * 16);
 
 // Per permuted position k (local index q = k − k_begin): where the block's
 // points and neighbour list live.  Points of position k are the contiguous

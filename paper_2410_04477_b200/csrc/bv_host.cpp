@@ -234,6 +234,24 @@ bool theta_valid(const double* th) {
   return true;
 }
 
+// ν-only table of the x > 2 K_ν evaluators (bessel_k.cuh), long double:
+//   [0, 28):  cosh(t_k) − 1,  [28, 56): cosh(ν t_k)      (t_k = 0.15 k, trapezoid)
+//   [56, 76): a_j = Π_{i≤j} (4ν² − (2i−1)²) / (8i)        (asymptotic series in 1/x)
+void fill_nu_table(double* tab, double nu) {
+  const long double ln = (long double)nu;
+  for (int k = 1; k <= bv::kNuTrapNodes; ++k) {
+    const long double t = 0.15L * (long double)k;
+    tab[k - 1] = (double)(std::cosh(t) - 1.0L);
+    tab[bv::kNuTrapNodes + k - 1] = (double)std::cosh(ln * t);
+  }
+  long double a = 1.0L;
+  for (int j = 1; j <= bv::kNuAsymTerms; ++j) {
+    const long double o = 2.0L * j - 1.0L;
+    a *= (4.0L * ln * ln - o * o) / (8.0L * j);
+    tab[2 * bv::kNuTrapNodes + j - 1] = (double)a;
+  }
+}
+
 void fill_theta(bv::Theta& t, const double* th) {
   std::memset(&t, 0, sizeof(t));
   t.sigma2 = th[0];
@@ -248,6 +266,15 @@ void fill_theta(bv::Theta& t, const double* th) {
     t.c_nu = (double)((long double)th[0] * std::pow(2.0L, 1.0L - ln) / std::tgamma(ln));
     fill_general_nu(t, th[2]);
   }
+}
+
+// θ into the pinned slot buffer: Theta in slot 0, the ν table right after it; `dev` = the
+// device copy's base (the table's device address goes into Theta::nutab)
+void fill_theta_buf(bv::Theta* host, const bv::Theta* dev, const double* th) {
+  fill_theta(*host, th);
+  double* tab = reinterpret_cast<double*>(host + 1);
+  host->nutab = reinterpret_cast<const double*>(dev + 1);
+  if (host->kind == bv::kNuGeneral) fill_nu_table(tab, th[2]);
 }
 
 void release(bv_handle* h) {
@@ -586,14 +613,14 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   TRY(upload(h, &h->d_perm_of_id, perm_of_id.data(), perm_of_id.size()));
   h->h_perm_of_id = perm_of_id;
   TRY(upload<double>(h, &h->d_y_stage, nullptr, (size_t)n));
-  TRY(upload<bv::Theta>(h, &h->d_theta, nullptr, 1));
+  TRY(upload<bv::Theta>(h, &h->d_theta, nullptr, bv::kThetaSlots));
   TRY(upload<double>(h, &h->d_u, nullptr, (size_t)h->nq));
   TRY(upload<double>(h, &h->d_d, nullptr, (size_t)h->nq));
   TRY(upload<unsigned long long>(h, &h->d_acc, nullptr, bv::kAccSlots));
   TRY(upload<unsigned long long>(h, &h->d_min, nullptr, 1));
-  TRYC(cudaMallocHost((void**)&h->h_theta, sizeof(bv::Theta)));
+  TRYC(cudaMallocHost((void**)&h->h_theta, sizeof(bv::Theta) * bv::kThetaSlots));
   TRYC(cudaMallocHost((void**)&h->h_acc, sizeof(unsigned long long) * bv::kAccSlots));
-  std::memset(h->h_theta, 0, sizeof(bv::Theta));
+  std::memset(h->h_theta, 0, sizeof(bv::Theta) * bv::kThetaSlots);
   TRY(upload(h, &h->d_tabs, slot_tables.tabs.data(), slot_tables.tabs.size()));
   TRY(upload(h, &h->d_tab_off, slot_tables.off.data(), slot_tables.off.size()));
   {
@@ -630,7 +657,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   //   exact term atomically) → [ncclAllReduce] → result to the host.
   for (int kind = 0; kind < 4; ++kind) {
     TRYC(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    cudaError_t e = cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta), cudaMemcpyHostToDevice, h->stream);
+    cudaError_t e = cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta) * bv::kThetaSlots,
+                                    cudaMemcpyHostToDevice, h->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->d_acc, 0, sizeof(unsigned long long) * 7, h->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->d_acc + 7, 0xff, sizeof(unsigned long long), h->stream);
     if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k0, h->stream, cudaEventRecordExternal);
@@ -690,7 +718,7 @@ static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
   if (!theta || !loglik) return fail(h, BV_EINVAL, "NULL argument");
   if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
   BV_CUDA(h, cudaSetDevice(h->device));
-  fill_theta(*h->h_theta, theta);
+  fill_theta_buf(h->h_theta, h->d_theta, theta);
   BV_CUDA(h, cudaGraphLaunch(h->exec[h->h_theta->kind], h->stream));
   BV_CUDA(h, cudaStreamSynchronize(h->stream));
   const unsigned long long* acc = h->h_acc;
@@ -894,8 +922,8 @@ bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp
   PCALL(cudaMemcpyAsync(d_nbr, nbr.data(), sizeof(int32_t) * nbr.size(), cudaMemcpyHostToDevice, st));
   PCALL(cudaMemcpyAsync(d_desc, desc.data(), sizeof(bv::BlockDesc) * bc, cudaMemcpyHostToDevice, st));
   PCALL(cudaMemcpyAsync(d_coff, coff.data(), sizeof(int64_t) * coff.size(), cudaMemcpyHostToDevice, st));
-  fill_theta(*h->h_theta, theta);
-  PCALL(cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta), cudaMemcpyHostToDevice, st));
+  fill_theta_buf(h->h_theta, h->d_theta, theta);
+  PCALL(cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta) * bv::kThetaSlots, cudaMemcpyHostToDevice, st));
   PCALL(bv::prepare_predict(std::max<size_t>(smax, 1024)));
   PCALL(bv::launch_predict(bc, smax, st, h->d_pts, d_np, d_nbr, d_desc, h->d_theta, d_coff, d_mean, d_var, d_cov,
                            d_status));

@@ -53,8 +53,11 @@ def full_parity(p, theta, label):
 
 
 @pytest.mark.parametrize("theta", [(1.0, 0.078809, 0.5), (1.0, 0.078809, 1.5), (1.0, 0.078809, 2.5),
-                                   (1.3, 0.05, 0.83), (0.8, 0.03, 1.0)])
+                                   (1.3, 0.05, 0.83), (0.8, 0.03, 1.0),
+                                   (1.0, 0.004, 1.7), (1.3, 0.3, 0.35), (0.7, 0.02, 2.9)])
 def test_c1_full_parity(theta):
+    """Closed-form ν and general ν across all three K_ν regimes of the device evaluator
+    (Temme x ≤ 2, trapezoid 2 < x ≤ 22, asymptotic x > 22: β = 0.004 puts most pairs there)."""
     p = sim_plan("c1", theta)
     full_parity(p, theta, f"c1 {theta}")
 

@@ -73,5 +73,10 @@ def test_mle_gpu_matches_oracle_path():
     ro = fit(oracle_ll(p), max_evals=300)
     bv.close()
     print("gpu", rg["theta"], rg["loglik"], rg["n_evals"], "oracle", ro["theta"], ro["loglik"], ro["n_evals"])
+    # both stop on the same relative-Δℓ rule (1e-7): the maxima agree to that resolution, and θ̂
+    # to what that flat a likelihood determines (the proposals diverge once ℓ differs in its
+    # 13th digit, so θ̂ is not expected to agree bitwise)
     assert abs(rg["loglik"] - ro["loglik"]) <= 1e-9 * abs(ro["loglik"])
-    np.testing.assert_allclose(rg["theta"], ro["theta"], rtol=1e-5)
+    np.testing.assert_allclose(rg["theta"], ro["theta"], rtol=1e-3)
+    cross = oracle_ll(p)(rg["theta"])
+    assert cross >= ro["loglik"] - 2e-7 * abs(ro["loglik"])
