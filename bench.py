@@ -269,6 +269,47 @@ def run_mle(args):
     return 0
 
 
+def run_predict(args):
+    """Alg. 2 at the config's scale: n* = n/10 new locations (same
+    distribution), bc* = bc/10 prediction blocks, the config's m.  value = predicted points per
+    second (mean + variance + block covariances), device-timed around bv_predict (host marshalling
+    of the prediction plan included — the paper predicts once per fit)."""
+    import torch
+    import paper_2410_04477_b200 as bvl
+    from paper_2410_04477_b200 import build as bvbuild
+    torch.cuda.set_device(0)
+    bvbuild.build()
+    c = workload(args.config)
+    plan = bvgen.cached_plan(args.config, m=args.m)
+    n_new, bc_new = max(1, plan.n // 10), max(1, plan.bc // 10)
+    new = bvgen.locations(c["cfg"] + 50, n_new, plan.d)
+    pp = bvgen.make_pred_plan(plan.locs, new, bc_new, plan.m)
+    theta = tuple(c["theta"])
+    bv = bvl.BlockVecchia(plan, device=0)
+    for _ in range(max(1, args.warmup)):
+        bv.predict(theta, pp)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        bv.predict(theta, pp, want_cov=True)
+        ts.append(time.perf_counter() - t)
+    bv.close()
+    lsz = np.bincount(pp.block_id, minlength=bc_new)
+    N = (lsz + plan.m).astype(np.float64)
+    flops = float(np.sum((plan.m ** 3) / 3.0 + plan.m ** 2 * lsz + plan.m * lsz * lsz))  # m eliminated columns
+    sec = float(np.median(ts))
+    out = {"metric": "block-Vecchia prediction (Alg. 2): predicted points/sec", "value": n_new / sec,
+           "unit": "points/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * sec,
+           "higher_is_better": True, "scaling": "none", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{args.config} prediction: n*={n_new:,} new points, bc*={bc_new:,} blocks, "
+                                  f"m={plan.m}, theta={theta}", "n_train": plan.n, "n_new": n_new, "bc_new": bc_new,
+                      "m": plan.m, "max_joint": int(N.max())},
+           "fp64_tflops": flops / sec / 1e12, "note": "wall time of bv_predict incl. host-side plan marshalling"}
+    print(json.dumps(out))
+    return 0
+
+
 def config_block(args, c, plan):
     return {"workload": f"{args.config}: n={plan.n:,} {plan.d}D, bc={plan.bc:,} K-means blocks, m={plan.m}, "
                         f"random ordering, Matern theta={tuple(c['theta'])}",
@@ -289,6 +330,8 @@ def main():
     ap.add_argument("--no-ablation", action="store_true", help="skip the factorisation-only ablation leg")
     ap.add_argument("--ablation-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--mle", action="store_true", help="c2 workload: a full MLE fit (hundreds of evaluations)")
+    ap.add_argument("--predict", action="store_true",
+                    help="Alg. 2 block prediction on the config's plan (new points = n/10, blocks = bc/10)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -296,6 +339,8 @@ def main():
         return run_ablation_child(args)
     if args.mle:
         return run_mle(args)
+    if args.predict:
+        return run_predict(args)
 
     import torch
     import paper_2410_04477_b200 as bvl
