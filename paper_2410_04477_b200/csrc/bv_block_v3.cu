@@ -401,8 +401,14 @@ constexpr int kV3GenUnroll = BV_V3_GEN_UNROLL;  // half-tiles in flight per upda
 #define BV_MINB_TINY 5
 #endif
 constexpr int v3_minb(int maxt) {
-  return kW == 4 ? (maxt <= 2 ? BV_MINB_TINY : maxt <= 5 ? BV_MINB_SMALL : 4) : (kW <= 6 ? 3 : 2);
+  return maxt >= 16 ? 2 : kW == 4 ? (maxt <= 2 ? BV_MINB_TINY : maxt <= 5 ? BV_MINB_SMALL : 4) : (kW <= 6 ? 3 : 2);
 }
+// Joint sizes beyond what shared memory holds (TI > 37, N > 295: the paper's
+// conditioning sets reach 420-450) keep the same schedule
+// with the tile slots in a global-memory scratch (L1/L2-resident) instead of
+// shared memory: MAXT ∈ {16, 20} (TI ≤ 61, N ≤ 480), persistent CTAs (the
+// scratch is gridDim × cap slots).  GS = "global slots".
+constexpr int kGsMaxT = 16;
 
 template <int MAXT, int KIND>
 __global__ void __launch_bounds__(kNT, v3_minb(MAXT))
@@ -411,10 +417,12 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
                    const Theta* __restrict__ theta_dev, const int16_t* __restrict__ tabs,
                    const int32_t* __restrict__ tab_off, const double* __restrict__ exp_tab, int TImax, int cap,
                    double* __restrict__ out_u, double* __restrict__ out_d, unsigned long long* __restrict__ acc,
-                   int k_begin) {
+                   int k_begin, double* __restrict__ gslots, int nblocks) {
+  constexpr bool GS = MAXT >= kGsMaxT;
   extern __shared__ __align__(16) double smem[];
-  const Layout Ly(TImax, cap);
-  const int q = list[blockIdx.x];
+  const Layout Ly(TImax, GS ? 0 : cap);
+  for (int bidx = blockIdx.x; bidx < (GS ? nblocks : (int)blockIdx.x + 1); bidx += gridDim.x) {
+  const int q = list[bidx];
   const BlockDesc ds = desc[q];
   const int m = ds.m, l = ds.l, N = m + l;
   const int TJ = (N + 7) >> 3;  // column panels
@@ -430,7 +438,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   double* misc = smem + Ly.misc;
   Theta* ths = reinterpret_cast<Theta*>(smem + Ly.theta);
   double* etab = smem + Ly.etab;
-  double* slots = smem + Ly.slots;
+  double* slots = GS ? gslots + (size_t)blockIdx.x * cap * 64 : smem + Ly.slots;
   int16_t* tab = reinterpret_cast<int16_t*>(smem + Ly.tab);
 
   // a1/a2: θ, gathered points (neighbours first), slot table, exp table
@@ -612,7 +620,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     if (MAXT >= n) u_gemm<(MAXT >= n ? n : 1), MAXT>(S, slots, tab, TI, J, uw, lane); \
     break;
           BV_NS(1) BV_NS(2) BV_NS(3) BV_NS(4) BV_NS(5) BV_NS(6) BV_NS(7) BV_NS(8) BV_NS(9) BV_NS(10) BV_NS(11)
-          BV_NS(12)
+          BV_NS(12) BV_NS(13) BV_NS(14) BV_NS(15) BV_NS(16) BV_NS(17) BV_NS(18) BV_NS(19) BV_NS(20)
 #undef BV_NS
           default: break;
         }
@@ -731,6 +739,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     out_d[q] = logdet;
     accumulate_term(acc, c, st, k_begin + q);
   }
+  if (GS) __syncthreads();  // the next block reuses shared memory and the scratch
+  }
 }
 
 }  // namespace v3
@@ -753,7 +763,7 @@ int debug_v3_cycles(unsigned long long* out, int reset) {
 
 int v3_maxt_for(int TI) {
   const int need = (TI - 1 + (v3::kW - 2)) / (v3::kW - 1);  // panel J+1 tiles I ≥ J+1 over the update warps
-  const int opts[] = {1, 2, 3, 4, 5, 6, 8, 10, 12};
+  const int opts[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20};
   for (int o : opts)
     if (o >= (need < 1 ? 1 : need)) return o;
   return -1;
@@ -762,8 +772,10 @@ int v3_maxt_for(int TI) {
 #ifndef BV_MIN_SMEM  // A/B only: pad the dynamic shared memory to cap resident CTAs per SM
 #define BV_MIN_SMEM 0
 #endif
+bool v3_global_slots(int TI) { return v3_maxt_for(TI) >= v3::kGsMaxT; }
+
 size_t v3_smem_bytes(int TImax, int cap) {
-  const size_t b = (size_t)v3::Layout(TImax, cap).total_bytes;
+  const size_t b = (size_t)v3::Layout(TImax, v3_global_slots(TImax) ? 0 : cap).total_bytes;
 #if BV_MIN_SMEM > 0
   return b < (size_t)BV_MIN_SMEM ? (size_t)BV_MIN_SMEM : b;
 #else
@@ -795,6 +807,8 @@ cudaError_t prepare_block_v3(size_t max_smem) {
   if (e == cudaSuccess) e = v3_prep<8>(max_smem);
   if (e == cudaSuccess) e = v3_prep<10>(max_smem);
   if (e == cudaSuccess) e = v3_prep<12>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<16>(max_smem);
+  if (e == cudaSuccess) e = v3_prep<20>(max_smem);
   return e;
 }
 
@@ -802,10 +816,10 @@ template <int MAXT>
 static void v3_launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, const PointRec* pts,
                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                            const int16_t* tabs, const int32_t* tab_off, const double* etab, int TImax, int cap,
-                           double* u, double* d, unsigned long long* acc, int k_begin) {
+                           double* u, double* d, unsigned long long* acc, int k_begin, double* gslots, int grid) {
 #define BV_K(KD)                                                                                             \
-  v3::bv_block_v3_kernel<MAXT, KD><<<nblocks, v3::kNT, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, \
-                                                                  TImax, cap, u, d, acc, k_begin)
+  v3::bv_block_v3_kernel<MAXT, KD><<<grid, v3::kNT, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, \
+                                                               TImax, cap, u, d, acc, k_begin, gslots, nblocks)
   switch (kind) {
     case 0: BV_K(0); break;
     case 1: BV_K(1); break;
@@ -818,16 +832,17 @@ static void v3_launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, c
 cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            unsigned long long* acc, int k_begin) {
+                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid) {
   if (nblocks == 0) return cudaSuccess;
   const size_t smem = v3_smem_bytes(TImax, cap);
+  const int grid = v3_global_slots(TImax) ? (nblocks < gs_grid ? nblocks : gs_grid) : nblocks;
   switch (v3_maxt_for(TImax)) {
 #define BV_MT(MT)                                                                                          \
   case MT:                                                                                                 \
     v3_launch_kind<MT>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, \
-                       acc, k_begin);                                                                      \
+                       acc, k_begin, gslots, grid);                                                        \
     break;
-    BV_MT(1) BV_MT(2) BV_MT(3) BV_MT(4) BV_MT(5) BV_MT(6) BV_MT(8) BV_MT(10) BV_MT(12)
+    BV_MT(1) BV_MT(2) BV_MT(3) BV_MT(4) BV_MT(5) BV_MT(6) BV_MT(8) BV_MT(10) BV_MT(12) BV_MT(16) BV_MT(20)
 #undef BV_MT
     default: return cudaErrorInvalidValue;
   }

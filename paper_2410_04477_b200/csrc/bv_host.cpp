@@ -46,7 +46,8 @@ cudaError_t prepare_block_v3(size_t max_smem);
 cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            unsigned long long* acc, int k_begin);
+                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid);
+bool v3_global_slots(int TI);
 int debug_phase_cycles(unsigned long long* out, int reset);
 int debug_v3_cycles(unsigned long long* out, int reset);
 size_t v2_smem_bytes(int TImax, int cap);
@@ -64,6 +65,7 @@ constexpr size_t kSmemOptin = 232448;  // B200 per-block opt-in shared memory
 struct Bucket {
   int Nmax, count, offset;  // v1: Nmax = joint size bound; v2: Nmax = tile rows TI
   int cap;                  // v2: L slots for this TI
+  size_t gs_off = 0;        // v3 with global slots (TI > 37): this bucket's scratch offset (doubles)
 };
 
 // Slot tables for the v2 kernel (bv_block_v2.cu).  Every tile of column K
@@ -159,6 +161,8 @@ struct bv_handle {
   double* d_y_stage = nullptr;
   int16_t* d_tabs = nullptr;
   double* d_exptab = nullptr;
+  double* d_gslots = nullptr;  // tile-slot scratch of the global-slot buckets (joint sizes > 295)
+  int gs_grid = 0;             // persistent CTAs per global-slot bucket launch
   int32_t* d_tab_off = nullptr;
   bool use_v1 = false, use_v2 = false;
   bv::Theta* h_theta = nullptr;            // pinned
@@ -287,7 +291,7 @@ void release(bv_handle* h) {
     h->graph[k] = nullptr;
   }
   if (h->comm) ncclCommDestroy(h->comm);
-  void* dev[] = {h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d,
+  void* dev[] = {h->d_gslots, h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d,
                  h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
   for (void* p : dev)
     if (p) cudaFree(p);
@@ -468,8 +472,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     }
     SlotTables st;
     st.v3 = !use_v2;
-    st.build(48);
-    while (N + 1 < 8 * 48) {
+    st.build(64);
+    while (N + 1 < 8 * 64) {
       const int TI = (N + 1 + 8) >> 3;
       const size_t sm = use_v2 ? bv::v2_smem_bytes(TI, st.cap[TI]) : bv::v3_smem_bytes(TI, st.cap[TI]);
       const int mt = use_v2 ? bv::v2_maxt_for(TI) : bv::v3_maxt_for(TI);
@@ -588,6 +592,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   slot_tables.build(TImax_all);
   int maxN = 8;
   size_t max_smem = 0;
+  size_t gs_total = 0;
   for (int32_t i = 0; i < h->nq;) {
     int32_t j = i;
     while (j < h->nq && bkey(list[j]) == bkey(list[i])) ++j;
@@ -600,12 +605,22 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     } else {
       const int TI = bkey(list[i]);
       h->buckets.push_back(Bucket{TI, j - i, i, slot_tables.cap[TI]});
+      if (!use_v2 && bv::v3_global_slots(TI)) {
+        if (h->gs_grid == 0) {
+          int sms = 148;
+          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+          h->gs_grid = 2 * sms;
+        }
+        h->buckets.back().gs_off = gs_total;
+        gs_total += (size_t)std::min(j - i, h->gs_grid) * slot_tables.cap[TI] * 64;
+      }
       max_smem = std::max(max_smem, use_v2 ? bv::v2_smem_bytes(TI, slot_tables.cap[TI])
                                            : bv::v3_smem_bytes(TI, slot_tables.cap[TI]));
     }
     i = j;
   }
 
+  if (gs_total > 0) TRY(upload<double>(h, &h->d_gslots, nullptr, gs_total));
   TRY(upload(h, &h->d_pts, pts.data(), pts.size()));
   TRY(upload(h, &h->d_nbr, nbr.data(), nbr.size()));
   TRY(upload(h, &h->d_desc, desc.data(), desc.size()));
@@ -681,7 +696,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
       else
         e = bv::launch_block_v3(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
                                 h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
-                                h->d_d, h->d_acc, h->kb);
+                                h->d_d, h->d_acc, h->kb, h->d_gslots ? h->d_gslots + b.gs_off : nullptr,
+                                h->gs_grid);
     }
     for (int b = 0; b < nbr_streams && e == cudaSuccess; ++b) {
       e = cudaEventRecord(h->join_ev[b], h->side[b]);

@@ -138,6 +138,8 @@ def test_c5_shaped_m200_sampled_parity():
     (700, 7, 100, 2),      # large blocks (N ≈ 200)
     (64, 2, 70, 2),        # second block conditions on all of the first (m > l_1)
     (600, 6, 180, 2),      # joint sizes up to ~280 (c5 at m = 200 reaches 263): one CTA per SM
+    (900, 6, 300, 2),      # joint sizes ~450 (the paper's cs = 420-450): tile slots in global scratch
+    (700, 7, 330, 3),      # 3D, joint sizes ~430, persistent CTAs over the global-slot bucket
 ])
 def test_edge_shapes_parity(n, bc, m, d):
     theta = (1.2, 0.09, 1.5)
@@ -225,11 +227,12 @@ def test_generating_model_on_gpu():
 
 
 def test_joint_size_beyond_limit_rejected():
-    """N = m + l above the largest joint size the shared-memory layout holds (295) → BV_EINVAL naming
-    the first offending position, never a silent fallback."""
-    p = bvgen.make_plan("c1", n=1200, bc=3, m=300, cfg=33)
+    """N = m + l above the largest joint size this build supports (480: shared-memory slots to 295,
+    global-memory slots to 480) → BV_EINVAL naming the first offending position, never a silent
+    fallback."""
+    p = bvgen.make_plan("c1", n=1200, bc=2, m=400, cfg=33)
     l, mk = p.block_sizes()
-    assert (l + mk).max() > 295
+    assert (l + mk).max() > 480
     with pytest.raises(BVError) as ei:
         BlockVecchia(p, device=0)
     assert ei.value.status == 2 and "largest joint size" in str(ei.value)
