@@ -363,19 +363,25 @@ __device__ __forceinline__ double yrow_sq(double2 d, int J, int t, int m, int N)
 
 // Update-warp GEMM for NS tiles I = J+1+(u−1)+3s (warp 1's first tile is the
 // next diagonal tile): S(s) += Σ_{K<J} L(I,K) L(J+1,K)ᵀ.
+__device__ __forceinline__ const double* slot_at(const double* base, unsigned slot) {
+  return reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) + (slot << 9));  // 64 doubles per slot
+}
+
 template <int NS, int MAXT>
 __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
                                        int uw, int lane) {
-  const int16_t* tJ = tab + (J + 1) * TI;
-  const int16_t* tI[NS];
+  // slot s of this lane's fragment pair: one shift-add from an unsigned 16-bit slot index
+  const double* sl = slots + 2 * lane;
+  const uint16_t* tJ = reinterpret_cast<const uint16_t*>(tab) + (J + 1) * TI;
+  const uint16_t* tI[NS];
 #pragma unroll
-  for (int s = 0; s < NS; ++s) tI[s] = tab + (J + uw + (kW - 1) * s) * TI;
+  for (int s = 0; s < NS; ++s) tI[s] = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (kW - 1) * s) * TI;
 #pragma unroll 2
   for (int K = 0; K < J; ++K) {
-    const double2 b = lds2(slots + 64 * tJ[K] + 2 * lane);
+    const double2 b = lds2(slot_at(sl, tJ[K]));
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      const double2 a = lds2(slots + 64 * tI[s][K] + 2 * lane);
+      const double2 a = lds2(slot_at(sl, tI[s][K]));
       dmma884(S[s][0], S[s][1], a.x, b.x);
       dmma884(S[s][0], S[s][1], a.y, b.y);
     }
@@ -697,12 +703,13 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       bar_sync(kBarF, kNT);  // the chain warp published L(J+1,J)
       P3_ADD(10, u10);
       P3_T(u11);
-      const double2 b = lds2(slots + 64 * tab[(J + 1) * TI + J] + 2 * lane);
+      const uint16_t* tabu = reinterpret_cast<const uint16_t*>(tab);
+      const double2 b = lds2(slot_at(slots + 2 * lane, tabu[(J + 1) * TI + J]));
 #pragma unroll
       for (int s = 0; s < MAXT; ++s) {
         const int I = J + uw + (kW - 1) * s;
         if (I < TI && I > J + 1) {  // the diagonal tile's last term is the chain warp's
-          const double2 a = lds2(slots + 64 * tab[I * TI + J] + 2 * lane);
+          const double2 a = lds2(slot_at(slots + 2 * lane, tabu[I * TI + J]));
           dmma884(S[s][0], S[s][1], a.x, b.x);
           dmma884(S[s][0], S[s][1], a.y, b.y);
           double* cp = slots + 64 * tab[I * TI + J + 1] + 8 * g + 2 * t;
