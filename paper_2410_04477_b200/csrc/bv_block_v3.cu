@@ -366,6 +366,9 @@ __device__ __forceinline__ double yrow_sq(double2 d, int J, int t, int m, int N)
 __device__ __forceinline__ const double* slot_at(const double* base, unsigned slot) {
   return reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) + (slot << 9));  // 64 doubles per slot
 }
+__device__ __forceinline__ double* slot_at(double* base, unsigned slot) {
+  return reinterpret_cast<double*>(reinterpret_cast<char*>(base) + (slot << 9));
+}
 
 template <int NS, int MAXT>
 __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
@@ -446,6 +449,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   double* etab = smem + Ly.etab;
   double* slots = GS ? gslots + (size_t)blockIdx.x * cap * 64 : smem + Ly.slots;
   int16_t* tab = reinterpret_cast<int16_t*>(smem + Ly.tab);
+  const uint16_t* tabu = reinterpret_cast<const uint16_t*>(tab);  // slot indices, unsigned: one shift-add per address
 
   // a1/a2: θ, gathered points (neighbours first), slot table, exp table
   if (tid < 64) etab[tid] = exp_tab[tid];
@@ -537,7 +541,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
               if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
           }
 #else
-          const double2 d = tile_trsm(slots + 64 * tab[TJ * TI + J], bi, bl, g, t, refine);
+          const double2 d = tile_trsm(slot_at(slots, tabu[TJ * TI + J]), bi, bl, g, t, refine);
           if (g == (N & 7)) qd_t += yrow_sq(d, J, t, m, N);
 #endif
         }
@@ -545,7 +549,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       }
       P3_T(t3);
       // L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ (a5/a6)
-      double* tj = slots + 64 * tab[(J + 1) * TI + J];
+      double* tj = slot_at(slots, tabu[(J + 1) * TI + J]);
       {
 #if BV_TRSM == 0
         double* row = tj + 8 * (lane & 7);  // row i = lane & 7 (lanes 8..31 shadow)
@@ -612,7 +616,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
             double v = matern_kind<KIND>(sqdist(P[r], pc), th, etab);
             v = (r == N) ? pc.v : v;
             v = (cval && r <= N) ? v : 0.0;
-            double* dst = (h < 2) ? ptile : slots + 64 * tab[I * TI + J + 1];
+            double* dst = (h < 2) ? ptile : slot_at(slots, tabu[I * TI + J + 1]);
             dst[32 * (h & 1) + lane] = v;
           }
         }
@@ -683,13 +687,13 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         for (int I = J + uw + (uw == 1 ? kW - 1 : 0); I < TI; I += 2 * (kW - 1)) {
           const int I2 = I + kW - 1;
           if (I2 < TI) {
-            double* const tl[2] = {slots + 64 * tab[I * TI + J], slots + 64 * tab[I2 * TI + J]};
+            double* const tl[2] = {slot_at(slots, tabu[I * TI + J]), slot_at(slots, tabu[I2 * TI + J])};
             double2 d[2];
             tile_trsm_n<2>(tl, bi, bl, g, t, d, refine);
             if (8 * I + g == N) qd_u += yrow_sq(d[0], J, t, m, N);  // the y row (a8)
             if (8 * I2 + g == N) qd_u += yrow_sq(d[1], J, t, m, N);
           } else {
-            const double2 d = tile_trsm(slots + 64 * tab[I * TI + J], bi, bl, g, t, refine);
+            const double2 d = tile_trsm(slot_at(slots, tabu[I * TI + J]), bi, bl, g, t, refine);
             if (8 * I + g == N) qd_u += yrow_sq(d, J, t, m, N);
           }
         }
@@ -703,7 +707,6 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       bar_sync(kBarF, kNT);  // the chain warp published L(J+1,J)
       P3_ADD(10, u10);
       P3_T(u11);
-      const uint16_t* tabu = reinterpret_cast<const uint16_t*>(tab);
       const double2 b = lds2(slot_at(slots + 2 * lane, tabu[(J + 1) * TI + J]));
 #pragma unroll
       for (int s = 0; s < MAXT; ++s) {
@@ -712,7 +715,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           const double2 a = lds2(slot_at(slots + 2 * lane, tabu[I * TI + J]));
           dmma884(S[s][0], S[s][1], a.x, b.x);
           dmma884(S[s][0], S[s][1], a.y, b.y);
-          double* cp = slots + 64 * tab[I * TI + J + 1] + 8 * g + 2 * t;
+          double* cp = slot_at(slots + 8 * g + 2 * t, tabu[I * TI + J + 1]);
           const double2 av = lds2(cp);
           sts2(cp, av.x - S[s][0], av.y - S[s][1]);
         }
