@@ -159,9 +159,8 @@ struct Layout {
 template <int KIND>
 __device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec& pc, int r, int c, int N,
                                              const Theta& th, const double* tab64) {
-  double v = matern_kind<KIND>(sqdist(pr, pc), th, tab64);
-  v = (r == N) ? pc.v : v;
-  return (c >= N || r > N) ? 0.0 : v;
+  const double v = matern_kind<KIND>(sqdist(pr, pc), th, tab64);
+  return (r == N) ? pc.v : v;  // the y row; padding entries are 0 by construction (far points)
 }
 
 // Row solve x = c L_JJ⁻ᵀ against the published diagonal factor (row-major
@@ -457,7 +456,11 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     reinterpret_cast<double*>(ths)[tid] = reinterpret_cast<const double*>(theta_dev)[tid];
 #pragma unroll 1
   for (int i = tid; i < 8 * TI; i += kNT) {
-    PointRec r = {0.0, 0.0, 0.0, 0.0};
+    // padding rows/columns (i ≥ N, and the y row's own point): far-apart points, so every
+    // padding entry off the diagonal is exactly 0 from Eq. (7) itself (x > 708 → 0) and no
+    // per-entry validity select is needed; padding pivots are substituted in factor_tile
+    const double far = 1e30 * (double)(i + 1);
+    PointRec r = {far, far, far, 0.0};
     if (i < N) r = pts[(i < m) ? nbr[ds.nbr_off + i] : ds.pstart + (i - m)];
     P[i] = r;
   }
@@ -608,14 +611,12 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         {
           const int c = 8 * (J + 1) + (lane & 7);
           const PointRec pc = P[c];
-          const bool cval = c < N;
           const int nh = 2 * (TI - J - 1);
 #pragma unroll(kV3GenUnroll)
           for (int h = uw - 1; h < nh; h += kW - 1) {
             const int I = J + 1 + (h >> 1), r = 8 * I + 4 * (h & 1) + (lane >> 3);
             double v = matern_kind<KIND>(sqdist(P[r], pc), th, etab);
-            v = (r == N) ? pc.v : v;
-            v = (cval && r <= N) ? v : 0.0;
+            v = (r == N) ? pc.v : v;  // padding entries are 0 by construction (far points)
             double* dst = (h < 2) ? ptile : slot_at(slots, tabu[I * TI + J + 1]);
             dst[32 * (h & 1) + lane] = v;
           }
