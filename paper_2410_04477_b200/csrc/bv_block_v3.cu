@@ -612,9 +612,10 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           const int c = 8 * (J + 1) + (lane & 7);
           const PointRec pc = P[c];
           const int nh = 2 * (TI - J - 1);
+          const int r0 = 8 * (J + 1) + (lane >> 3);  // half-tile h covers rows r0 + 4h (+ lane/8)
 #pragma unroll(kV3GenUnroll)
           for (int h = uw - 1; h < nh; h += kW - 1) {
-            const int I = J + 1 + (h >> 1), r = 8 * I + 4 * (h & 1) + (lane >> 3);
+            const int I = J + 1 + (h >> 1), r = r0 + 4 * h;
             double v = matern_kind<KIND>(sqdist(P[r], pc), th, etab);
             v = (r == N) ? pc.v : v;  // padding entries are 0 by construction (far points)
             double* dst = (h < 2) ? ptile : slot_at(slots, tabu[I * TI + J + 1]);
