@@ -69,6 +69,10 @@ def lib():
                                        C.c_int, C.c_int, C.c_int32, C.c_int32,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32), C.c_uint32]
+            L.or_bv_loglik_jitter.restype = C.c_int
+            L.or_bv_loglik_jitter.argtypes = [C.c_int64, C.c_int, _d, _d, C.c_int32, _i32, _i32, _i64, _i32, _d,
+                                              C.c_int, C.c_int32, C.c_int32, _d, _d, _d, _d,
+                                              C.POINTER(C.c_double), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
             L.or_exact_loglik.restype = C.c_int
             L.or_exact_loglik.argtypes = [C.c_int64, C.c_int, _d, _d, _d, C.c_int, C.POINTER(C.c_double)]
             L.or_classic_vecchia.restype = C.c_int
@@ -164,6 +168,26 @@ def bv_loglik(plan, theta, long_double: bool = False, nthreads: int = 0, k_range
     if st:
         raise OracleError(st, fp.value)
     return {"loglik": ll.value, "u": u, "d": dd, "t": t}
+
+
+def bv_loglik_jitter(plan, theta, nthreads: int = 0):
+    """Alg. 1 with the optional jitter mode (reading G15b; SPEC.md:197,
+    :238 schedule with base_scale = σ²): a block whose POTRF fails is re-run with
+    ε·σ² added to the diagonal of Σcon and Σlk, ε = 1e-10, 1e-8, 1e-6 in turn.
+    Returns dict(loglik, u, d, t, eps (per block, 0 = none), events)."""
+    L = lib()
+    locs = _c(plan.locs, np.float64)
+    n, d = locs.shape
+    bc = int(plan.order.shape[0])
+    u, dd, t, eps = (np.zeros(bc) for _ in range(4))
+    ll, fp, ev = C.c_double(0.0), C.c_int32(-1), C.c_int32(0)
+    st = L.or_bv_loglik_jitter(n, d, locs, _c(plan.y, np.float64), bc, _c(plan.block_id, np.int32),
+                               _c(plan.order, np.int32), _c(plan.nbr_ptr, np.int64), _c(plan.nbr_idx, np.int32),
+                               _c(theta, np.float64), int(nthreads), 0, bc, u, dd, t, eps, C.byref(ll),
+                               C.byref(fp), C.byref(ev))
+    if st:
+        raise OracleError(st, fp.value)
+    return {"loglik": ll.value, "u": u, "d": dd, "t": t, "eps": eps, "events": ev.value}
 
 
 def exact_loglik(locs, y, theta, long_double: bool = False) -> float:

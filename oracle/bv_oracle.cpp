@@ -14,6 +14,8 @@
  *                        literally: POTRF, TRSM, TRSV, GEMM, GEMV, subtract,
  *                        POTRF, TRSV, dot, logdet, accumulate — nine separate
  *                        steps, NOT the fused joint Cholesky the GPU uses.
+ *   or_bv_loglik_jitter  the same with the optional jitter retry schedule
+ *                        (reading G15b).
  *   or_exact_loglik      Eq. (1), PAPER.md:62-67 (§1) — dense Cholesky.
  *   or_classic_vecchia   classic Vecchia = block size 1, PAPER.md:76-78, :83;
  *                        univariate conditionals solved by Gaussian
@@ -185,7 +187,8 @@ void build_block_lists(PlanView& P, const int32_t* block_id) {
 /* One block of Alg. 1, literally, at permuted position k.
  * Returns 0, or 3 if a POTRF failed (non-PD). */
 template <class R>
-int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R* d_out, uint32_t seed) {
+int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R* d_out, uint32_t seed,
+               R jit = R(0)) {
   const int32_t b = P.order[k];
   const int l = (int)(P.bptr[(size_t)b + 1] - P.bptr[b]);
   const int32_t* B = P.bidx.data() + P.bptr[b];
@@ -199,6 +202,7 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
   for (int a = 0; a < l; ++a)
     for (int c = 0; c < l; ++c)
       Slk[(size_t)a * l + c] = perturb_entry(matern<R>(dist<R>(loc(B[a]), loc(B[c]), d), sigma2, beta, nu), B[a], B[c], seed);
+  for (int a = 0; a < l; ++a) Slk[(size_t)a * l + a] += jit;  // optional jitter mode (reading G15b)
   // l.14  y_B, y_NN
   std::vector<R> yB(l), yN(m);
   for (int a = 0; a < l; ++a) yB[a] = R(P.y[B[a]]);
@@ -212,6 +216,7 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
     for (int a = 0; a < m; ++a)
       for (int c = 0; c < m; ++c)
         Scon[(size_t)a * m + c] = perturb_entry(matern<R>(dist<R>(loc(NN[a]), loc(NN[c]), d), sigma2, beta, nu), NN[a], NN[c], seed);
+    for (int a = 0; a < m; ++a) Scon[(size_t)a * m + a] += jit;  // reading G15b
     // l.13  Σcross ← K(s_NN, s_B)   (m×l, reading G8)
     std::vector<R> Scross((size_t)m * l);
     for (int a = 0; a < m; ++a)
@@ -264,7 +269,8 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
 template <class R>
 int bv_loglik_impl(PlanView& P, const int32_t* block_id, const double* theta, double* out_u, double* out_d,
                    double* out_t, double* out_loglik, int32_t* failed_pos, int nthreads, int k_begin, int k_end,
-                   double* out_loglik_ld_sum, uint32_t seed) {
+                   double* out_loglik_ld_sum, uint32_t seed, int jitter_mode = 0, double* out_eps = nullptr,
+                   int32_t* out_events = nullptr) {
   build_block_lists(P, block_id);
   const R sigma2 = R(theta[0]), beta = R(theta[1]), nu = R(theta[2]);
   const int nk = k_end - k_begin;
@@ -278,6 +284,20 @@ int bv_loglik_impl(PlanView& P, const int32_t* block_id, const double* theta, do
     const int32_t k = k_begin + q;
     R u = 0, d = 0;
     st[q] = alg1_block<R>(P, k, sigma2, beta, nu, &u, &d, seed);
+    // Optional jitter mode (reading G15b; SPEC.md:197 schedule with base_scale = σ²,
+    // SPEC.md:238): a block whose POTRF failed is re-run from scratch with
+    // ε·σ² added to every diagonal entry of Σcon and Σlk, ε = 1e-10, 1e-8, 1e-6
+    // in turn; the first ε that succeeds is kept.
+    double eps_used = 0.0;
+    if (jitter_mode && st[q] != 0) {
+      static const double kSched[3] = {1e-10, 1e-8, 1e-6};
+      for (int e = 0; e < 3 && st[q] != 0; ++e) {
+        st[q] = alg1_block<R>(P, k, sigma2, beta, nu, &u, &d, seed, R(kSched[e]) * sigma2);
+        eps_used = kSched[e];
+      }
+      if (st[q] != 0) eps_used = 0.0;
+    }
+    if (out_eps) out_eps[q] = eps_used;
     const int l = (int)(P.bptr[(size_t)P.order[k] + 1] - P.bptr[P.order[k]]);
     uu[q] = u;
     dd[q] = d;
@@ -287,6 +307,12 @@ int bv_loglik_impl(PlanView& P, const int32_t* block_id, const double* theta, do
   int32_t fail = -1;
   for (int q = 0; q < nk; ++q)
     if (st[q] != 0) { fail = k_begin + q; break; }
+  if (out_events) {
+    int32_t ev = 0;
+    if (out_eps)
+      for (int q = 0; q < nk; ++q) ev += (st[q] == 0 && out_eps[q] > 0.0) ? 1 : 0;
+    *out_events = ev;
+  }
   if (failed_pos) *failed_pos = fail;
   if (fail >= 0) {
     if (out_loglik) *out_loglik = -INFINITY;
@@ -389,6 +415,22 @@ int or_bv_loglik(int64_t n, int d, const double* locs, const double* y, int32_t 
                                        k_begin, k_end, nullptr, 0u);
   return bv_loglik_impl<double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads, k_begin,
                                 k_end, nullptr, perturb_seed);
+}
+
+/* Alg. 1 with the optional jitter mode (reading G15b): per block, the
+ * failed-POTRF retry schedule ε ∈ {1e-10, 1e-8, 1e-6}·σ² on the diagonal of
+ * Σcon and Σlk.  out_eps[q] = the ε used (0 = none); *events = blocks that
+ * needed one (SPEC.md:269 jitter_events).  FP64 only. */
+int or_bv_loglik_jitter(int64_t n, int d, const double* locs, const double* y, int32_t bc, const int32_t* block_id,
+                        const int32_t* order, const int64_t* nbr_ptr, const int32_t* nbr_idx, const double* theta,
+                        int nthreads, int32_t k_begin, int32_t k_end, double* out_u, double* out_d, double* out_t,
+                        double* out_eps, double* out_loglik, int32_t* failed_pos, int32_t* events) {
+  if (!theta_ok(theta) || n < 1 || (d != 2 && d != 3) || bc < 1 || k_begin < 0 || k_end > bc || k_begin > k_end ||
+      !out_eps || !events)
+    return 2;
+  PlanView P{n, d, locs, y, bc, order, nbr_ptr, nbr_idx, {}, {}};
+  return bv_loglik_impl<double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads, k_begin,
+                                k_end, nullptr, 0u, 1, out_eps, events);
 }
 
 /* Alg. 2: block-Vecchia prediction at n_new new locations.

@@ -318,3 +318,85 @@ def test_perturbed_replicas_measure_fp64_error_at_high_kappa():
     a = oracle.bv_loglik(p, theta, perturb_seed=1)
     b = oracle.bv_loglik(p, theta, perturb_seed=1)
     assert np.array_equal(a["t"], b["t"])  # deterministic
+
+
+# ------------------------------------------------------------------ optional jitter mode (reading G15b)
+def _exp_cov(A, B, theta):
+    """ν = 1/2 Matérn written out: σ² exp(−r/β) (Eq. (7) at ν = 1/2)."""
+    r = np.sqrt(((A[:, None, :] - B[None, :, :]) ** 2).sum(-1))
+    return theta[0] * np.exp(-r / theta[1])
+
+
+def _gauss_logpdf(S, y):
+    Lc = np.linalg.cholesky(S)
+    z = np.linalg.solve(Lc, y)
+    return -0.5 * (z @ z + 2.0 * np.log(np.diag(Lc)).sum() + len(y) * math.log(2 * math.pi))
+
+
+def _dup_plan(pos=4, n=200, bc=10, m=10):
+    p = small_plan(n=n, bc=bc, m=m, sim=False)
+    locs = p.locs.copy()
+    b = p.order[pos]
+    members = np.where(p.block_id == b)[0]
+    locs[members[1]] = locs[members[0]]
+    y = bvgen.normal(77, p.n)
+    y[members[1]] = y[members[0]] + 1e-6
+    return bvgen.Plan(locs, y, p.block_id, p.order, p.nbr_ptr, p.nbr_idx)
+
+
+def test_jitter_single_block_equals_exact_likelihood_with_nugget():
+    """bc = 1 with a repeated location: the jitter mode's first ε (1e-10)
+    makes ℓ the exact Eq. (1) likelihood of Σθ + 1e-10·σ²·I (numpy dense Cholesky)."""
+    theta = (1.3, 0.1, 0.5)
+    p = small_plan(n=60, bc=1, m=5, sim=False)
+    locs = p.locs.copy()
+    locs[7] = locs[3]
+    y = bvgen.normal(5, p.n)
+    y[7] = y[3] + 1e-5
+    q = bvgen.Plan(locs, y, p.block_id, p.order, p.nbr_ptr, p.nbr_idx)
+    with pytest.raises(oracle.OracleError):
+        oracle.bv_loglik(q, theta)
+    r = oracle.bv_loglik_jitter(q, theta)
+    S = _exp_cov(locs, locs, theta) + 1e-10 * theta[0] * np.eye(p.n)
+    ex = _gauss_logpdf(S, y)
+    assert r["events"] == 1 and r["eps"][0] == 1e-10
+    assert abs(r["loglik"] - ex) <= 1e-7 * abs(ex), (r["loglik"], ex)
+
+
+def test_jitter_blocks_equal_jittered_conditional_density():
+    """Multi-block plan, one repeated location: every block that needed jitter has
+    t_k = log p(y_NN, y_B) − log p(y_NN) under Σθ + ε·σ²·I (Eq. (4)'s conditional,
+    PAPER.md:161, formed from two dense log-densities, not Alg. 1's steps); every
+    other block is untouched (bitwise equal to Alg. 1 without jitter)."""
+    theta = (1.0, 0.1, 0.5)
+    q = _dup_plan()
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.bv_loglik(q, theta)
+    r = oracle.bv_loglik_jitter(q, theta)
+    jit = np.nonzero(r["eps"])[0]
+    assert r["events"] == len(jit) >= 1 and jit[0] == e.value.failed_position
+    assert set(r["eps"][jit]) <= {1e-10, 1e-8, 1e-6}
+    for k in range(q.bc):
+        B = np.sort(np.where(q.block_id == q.order[k])[0])
+        NN = q.nbr_idx[q.nbr_ptr[k]:q.nbr_ptr[k + 1]]
+        if r["eps"][k] == 0:
+            o = oracle.bv_loglik(q, theta, k_range=(k, k + 1))
+            assert o["t"][0] == r["t"][k]
+            continue
+        J = np.concatenate([NN, B])
+        SJ = _exp_cov(q.locs[J], q.locs[J], theta) + r["eps"][k] * theta[0] * np.eye(len(J))
+        want = _gauss_logpdf(SJ, q.y[J])
+        if len(NN):
+            want -= _gauss_logpdf(SJ[:len(NN), :len(NN)], q.y[NN])
+        assert abs(r["t"][k] - want) <= 1e-6 * (abs(want) + len(B)), (k, r["t"][k], want)
+    assert abs(r["loglik"] - r["t"].sum()) <= 1e-9 * abs(r["loglik"])
+
+
+def test_jitter_mode_is_identity_without_failures():
+    """No failing block → the jitter mode returns Alg. 1's result bitwise, 0 events."""
+    theta = THETAS[1]
+    p = small_plan(n=300, bc=12, m=15, theta=theta)
+    a = oracle.bv_loglik(p, theta)
+    b = oracle.bv_loglik_jitter(p, theta)
+    assert b["events"] == 0 and not b["eps"].any()
+    assert a["loglik"] == b["loglik"] and np.array_equal(a["t"], b["t"])
