@@ -108,6 +108,21 @@ bv_status bv_loglik(bv_handle* h, const double theta[3], double* loglik);
  * (host arrays of k_end - k_begin doubles; either may be NULL). */
 bv_status bv_loglik_terms(bv_handle* h, const double theta[3], double* loglik, double* logdet, double* quad);
 
+/* Optional jitter mode (off by default; reading G15b, SPEC.md:197,
+ * :238).  When enabled, a bv_loglik* evaluation in which some block is not
+ * positive definite recomputes each failed block with ε·σ² added to every
+ * diagonal entry of its joint matrix (the diagonals of Σcon and Σlk),
+ * ε = 1e-10, 1e-8, 1e-6 in turn, keeping the first that succeeds; only if
+ * one still fails does the call return BV_ENOTPD.  The retry runs off the
+ * captured graph and only after a failure, so evaluations without failures
+ * cost the same.  Blocks with joint size > 235 are not retried.  Collective
+ * when world > 1: set it identically on every rank.  Errors: BV_EINVAL (NULL). */
+bv_status bv_set_jitter(bv_handle* h, int32_t enable);
+
+/* Blocks (over all ranks) that needed jitter in the most recent evaluation
+ * (SPEC.md:269 jitter_events); 0 when the mode is off. */
+bv_status bv_jitter_events(const bv_handle* h, int64_t* events);
+
 /* This rank's contiguous range of permuted positions. */
 bv_status bv_owned_range(const bv_handle* h, int32_t* k_begin, int32_t* k_end);
 

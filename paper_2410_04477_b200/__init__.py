@@ -31,7 +31,7 @@ _NAMES = {2: "BV_EINVAL", 3: "BV_ENOTPD", 4: "BV_EIO", 5: "BV_ECUDA", 6: "BV_ENC
 EXPORTS = ["bv_version", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_owned_range",
            "bv_loglik_host_y", "bv_last_error", "bv_launches_per_eval", "bv_stream", "bv_last_kernel_ms", "bv_destroy", "bv_partition",
            "bv_fixed_encode", "bv_fixed_decode", "bv_predict", "bv_plan_kmeans", "bv_plan_block_nn",
-           "bv_plan_last_error"]
+           "bv_plan_last_error", "bv_set_jitter", "bv_jitter_events"]
 
 
 class BVError(RuntimeError):
@@ -77,6 +77,8 @@ def lib():
             L.bv_loglik.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
             L.bv_loglik_terms.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_void_p, C.c_void_p]
             L.bv_loglik_host_y.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
+            L.bv_set_jitter.argtypes = [C.c_void_p, C.c_int32]
+            L.bv_jitter_events.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
             L.bv_owned_range.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
             L.bv_last_error.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_char_p)]
             L.bv_launches_per_eval.restype = C.c_int32
@@ -99,7 +101,8 @@ def lib():
                                            C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
             L.bv_plan_last_error.restype = C.c_char_p
             for fn in ("bv_plan_kmeans", "bv_plan_block_nn", "bv_predict", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_loglik_host_y",
-                       "bv_owned_range", "bv_last_error", "bv_partition", "bv_fixed_encode"):
+                       "bv_owned_range", "bv_last_error", "bv_partition", "bv_fixed_encode", "bv_set_jitter",
+                       "bv_jitter_events"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
     return _lib
@@ -245,6 +248,17 @@ class BlockVecchia:
         out = C.c_double()
         self._check(self._L.bv_loglik_terms(self._h, th.ctypes.data, C.byref(out), _ptr(d), _ptr(u)))
         return out.value, d, u
+
+    def set_jitter(self, enable: bool = True):
+        """Optional jitter retry for non-PD blocks (bv_set_jitter; reading G15b)."""
+        self._check(self._L.bv_set_jitter(self._h, 1 if enable else 0))
+
+    @property
+    def jitter_events(self) -> int:
+        """Blocks that needed jitter in the last evaluation (bv_jitter_events)."""
+        ev = C.c_int64()
+        self._check(self._L.bv_jitter_events(self._h, C.byref(ev)))
+        return ev.value
 
     def loglik_host_y(self, y, theta) -> float:
         """End-to-end call: host y (global id order) copied in, ℓ back."""

@@ -47,12 +47,21 @@ def build(force: bool = False, verbose: bool = False, profile_phases: bool = Fal
     inc, libdir = nccl_dirs()
     tmp = out + f".tmp{os.getpid()}"
     extra = (["-DBV_PROFILE_PHASES"] if profile_phases else []) + [f"-D{d}" for d in defines]
-    cmd = (["nvcc", *ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-            "-Xptxas", "-v" if verbose else "-O3",
-            "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc, "-o", tmp]
-           + [os.path.join(CSRC, f) for f in SOURCES]
-           + ["-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}"])
-    subprocess.check_call(cmd)
+    flags = [*ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
+    # one nvcc per translation unit, in parallel (the v3 kernel's instantiations dominate), then link
+    objs = [f"{tmp}.{i}.o" for i in range(len(SOURCES))]
+    procs = [subprocess.Popen(["nvcc", *flags, "-c", os.path.join(CSRC, f), "-o", o]) for f, o in zip(SOURCES, objs)]
+    rcs = [p.wait() for p in procs]
+    try:
+        if any(rcs):
+            raise subprocess.CalledProcessError(max(rcs), "nvcc -c " + " ".join(SOURCES))
+        subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", tmp, *objs,
+                               "-L", libdir, "-l:libnccl.so.2", f"-Xlinker=-rpath,{libdir}"])
+    finally:
+        for o in objs:
+            if os.path.exists(o):
+                os.remove(o)
     os.replace(tmp, out)
     return out
 

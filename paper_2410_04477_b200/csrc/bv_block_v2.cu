@@ -448,7 +448,7 @@ bv_block_v2_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     const bool fail = misc[2] != 0.0;
     int st = fail ? kNotPD : kOk;
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
-    const double logdet = fail ? 0.0 : log(pm) + (double)pe * 0.69314718055994530942;  // d = Σ_{j≥m} log p_j
+    const double logdet = fail ? failed_d() : log(pm) + (double)pe * 0.69314718055994530942;  // d = Σ_{j≥m} log p_j
     const double quad = fail ? 0.0 : misc[1] + qd;
     if (!fail) {
       const double tk = -0.5 * (quad + logdet + (double)l * kLn2Pi);

@@ -739,7 +739,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     const bool fail = misc[2] != 0.0;
     int st = fail ? kNotPD : kOk;
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
-    const double logdet = fail ? 0.0 : misc[4];
+    const double logdet = fail ? failed_d() : misc[4];
     double quad = misc[1];
     for (int w = 1; w < kW; ++w) quad += misc[4 + w];  // fixed order: bitwise reproducible
     quad = fail ? 0.0 : quad;

@@ -55,6 +55,11 @@ constexpr double kPivotFloor = 1e-14;
 
 // Block status codes written by the kernels.
 enum BlockStatus : int32_t { kOk = 0, kNotPD = 1, kTermRange = 2 };
+// A block that failed with kNotPD writes d_k = NaN (a valid d_k is finite), so the
+// host's optional jitter retry (reading G15b) can list the failed positions.
+#ifdef __CUDACC__
+__device__ __forceinline__ double failed_d() { return __longlong_as_double(0x7ff8000000000000ll); }
+#endif
 
 // ---------------------------------------------------------------------------
 // Exact fixed-point block terms.  T = round(t·2⁶⁴) as a 192-bit

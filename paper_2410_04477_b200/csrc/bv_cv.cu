@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kCvWarps * 32) bv_cv_kernel(const PointRec* __
     const bool fail = bad || !(plast > pfloor) || !(plast <= 1.7976931348623157e308);
     int st = fail ? kNotPD : kOk;
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
-    const double d = fail ? 0.0 : log(plast);
+    const double d = fail ? failed_d() : log(plast);
     const double u = fail ? 0.0 : yk * yk / plast;
     if (!fail) {
       const double t = -0.5 * (u + d + kLn2Pi);

@@ -29,7 +29,7 @@ size_t v1_smem_bytes(int Nmax);
 cudaError_t prepare_block_v1(int Nmax);
 cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                             const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
-                            unsigned long long* acc, int k_begin);
+                            unsigned long long* acc, int k_begin, double jit = 0.0);
 cudaError_t launch_cv(int kind, int count, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                       const BlockDesc* desc, const int32_t* list, const Theta* th, const double* etab, double* u,
                       double* d, unsigned long long* acc, int k_begin);
@@ -174,6 +174,13 @@ struct bv_handle {
   std::vector<Bucket> buckets;
   std::string err;
   int32_t failed_pos = -1;
+  // optional jitter retry (reading G15b; off the hot path, never captured)
+  bool jitter = false;
+  int64_t jitter_events = 0;
+  std::vector<int32_t> h_N;                  // joint size N_q = l + m per local position
+  int32_t* d_jlist = nullptr;                // failed positions being retried
+  unsigned long long* d_jacc = nullptr;      // the retry's own accumulator (kAccSlots) + 3 allreduce slots
+  int v1_ready = 0;                          // largest N prepare_block_v1 was called for
 };
 
 namespace {
@@ -292,7 +299,7 @@ void release(bv_handle* h) {
   }
   if (h->comm) ncclCommDestroy(h->comm);
   void* dev[] = {h->d_gslots, h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d,
-                 h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
+                 h->d_jlist, h->d_jacc, h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (h->h_theta) cudaFreeHost(h->h_theta);
@@ -624,6 +631,8 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   TRY(upload(h, &h->d_pts, pts.data(), pts.size()));
   TRY(upload(h, &h->d_nbr, nbr.data(), nbr.size()));
   TRY(upload(h, &h->d_desc, desc.data(), desc.size()));
+  h->h_N.resize((size_t)h->nq);
+  for (int32_t q = 0; q < h->nq; ++q) h->h_N[q] = Nq(q);
   TRY(upload(h, &h->d_list, list.data(), list.size()));
   TRY(upload(h, &h->d_perm_of_id, perm_of_id.data(), perm_of_id.size()));
   h->h_perm_of_id = perm_of_id;
@@ -728,8 +737,90 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   return BV_OK;
 }
 
+// Optional jitter mode (reading G15b; SPEC.md:197, :238 schedule with
+// base_scale = σ²): after an evaluation in which some block failed, every
+// failed position (d_k = NaN) is recomputed from scratch by the v1 kernel with
+// ε·σ² on its joint diagonal, ε = 1e-10, 1e-8, 1e-6, the first success kept.
+// The retry's exact terms go to their own accumulator and are added slot-wise
+// to the evaluation's (integer sums: still order-independent).  Collective when
+// world > 1 (every rank sees the same global failure count and enters).
+constexpr bv_status kJitterDefer = (bv_status)-1;
+static bv_status jitter_retry(bv_handle* h, const unsigned long long* acc, double* loglik) {
+  static const double kSched[3] = {1e-10, 1e-8, 1e-6};
+  constexpr int kV1MaxN = 235;  // packed-lower v1 fits the 227 KB opt-in up to N = 235
+  std::vector<double> dh((size_t)h->nq);
+  if (h->nq > 0) BV_CUDA(h, cudaMemcpy(dh.data(), h->d_d, sizeof(double) * h->nq, cudaMemcpyDeviceToHost));
+  std::vector<int32_t> F;
+  for (int32_t q = 0; q < h->nq; ++q)
+    if (std::isnan(dh[(size_t)q])) F.push_back(q);
+  const uint64_t nan_local = F.size();
+  uint64_t sums[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // [0..5] retry chunk sums, [6] still failed, [7] events, [8] NaN
+  if (!F.empty()) {
+    if (!h->d_jlist) BV_CUDA(h, cudaMalloc(&h->d_jlist, sizeof(int32_t) * (size_t)h->nq));
+    if (!h->d_jacc) BV_CUDA(h, cudaMalloc(&h->d_jacc, sizeof(unsigned long long) * 9));
+    if (h->v1_ready == 0) {
+      BV_CUDA(h, bv::prepare_block_v1(kV1MaxN));
+      h->v1_ready = kV1MaxN;
+    }
+    const double s2 = h->h_theta->sigma2;
+    std::vector<int32_t> keep;  // blocks too large for v1 stay failed
+    std::vector<int32_t> R;
+    for (int32_t q : F) (h->h_N[(size_t)q] <= kV1MaxN ? R : keep).push_back(q);
+    for (int e = 0; e < 3 && !R.empty(); ++e) {
+      int Nmax = 1;
+      for (int32_t q : R) Nmax = std::max(Nmax, h->h_N[(size_t)q]);
+      unsigned long long a0[bv::kAccSlots] = {0, 0, 0, 0, 0, 0, 0, ~0ull};
+      BV_CUDA(h, cudaMemcpyAsync(h->d_jacc, a0, sizeof(a0), cudaMemcpyHostToDevice, h->stream));
+      BV_CUDA(h, cudaMemcpyAsync(h->d_jlist, R.data(), sizeof(int32_t) * R.size(), cudaMemcpyHostToDevice,
+                                 h->stream));
+      BV_CUDA(h, bv::launch_block_v1((int)R.size(), Nmax, h->stream, h->d_pts, h->d_nbr, h->d_desc, h->d_jlist,
+                                     h->d_theta, h->d_u, h->d_d, h->d_jacc, h->kb, kSched[e] * s2));
+      BV_CUDA(h, cudaMemcpyAsync(a0, h->d_jacc, sizeof(a0), cudaMemcpyDeviceToHost, h->stream));
+      BV_CUDA(h, cudaMemcpyAsync(dh.data(), h->d_d, sizeof(double) * h->nq, cudaMemcpyDeviceToHost, h->stream));
+      BV_CUDA(h, cudaStreamSynchronize(h->stream));
+      for (int i = 0; i < 6; ++i) sums[i] += a0[i];
+      std::vector<int32_t> R2;
+      for (int32_t q : R)
+        if (std::isnan(dh[(size_t)q])) R2.push_back(q);
+      sums[7] += R.size() - R2.size();
+      R.swap(R2);
+    }
+    keep.insert(keep.end(), R.begin(), R.end());
+    F.swap(keep);
+    sums[6] = F.size();
+  }
+  sums[8] = nan_local;
+  if (h->world > 1) {
+    if (!h->d_jacc) BV_CUDA(h, cudaMalloc(&h->d_jacc, sizeof(unsigned long long) * 9));
+    BV_CUDA(h, cudaMemcpyAsync(h->d_jacc, sums, sizeof(sums), cudaMemcpyHostToDevice, h->stream));
+    BV_NCCL(h, ncclAllReduce(h->d_jacc, h->d_jacc, 9, ncclUint64, ncclSum, h->comm, h->stream));
+    BV_CUDA(h, cudaMemcpyAsync(sums, h->d_jacc, sizeof(sums), cudaMemcpyDeviceToHost, h->stream));
+    BV_CUDA(h, cudaStreamSynchronize(h->stream));
+  }
+  if (sums[8] != acc[6]) return kJitterDefer;  // a non-NaN failure (term range): caller reports it
+  h->jitter_events = (int64_t)sums[7];
+  if (sums[6] != 0) {
+    unsigned long long mn = F.empty() ? ~0ull : ((unsigned long long)(h->kb + *std::min_element(F.begin(), F.end())));
+    if (h->world > 1) {
+      BV_CUDA(h, cudaMemcpyAsync(h->d_min, &mn, 8, cudaMemcpyHostToDevice, h->stream));
+      BV_NCCL(h, ncclAllReduce(h->d_min, h->d_min, 1, ncclUint64, ncclMin, h->comm, h->stream));
+      BV_CUDA(h, cudaMemcpyAsync(&mn, h->d_min, 8, cudaMemcpyDeviceToHost, h->stream));
+      BV_CUDA(h, cudaStreamSynchronize(h->stream));
+    }
+    h->failed_pos = (int32_t)mn;
+    *loglik = -INFINITY;
+    return fail(h, BV_ENOTPD, "block at position " + std::to_string(h->failed_pos) +
+                                  " is not positive definite after the jitter schedule");
+  }
+  uint64_t a6[6];
+  for (int i = 0; i < 6; ++i) a6[i] = acc[i] + sums[i];
+  *loglik = bv_fixed_decode(a6);
+  return BV_OK;
+}
+
 static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
   h->failed_pos = -1;
+  h->jitter_events = 0;
   h->err.clear();
   if (!theta || !loglik) return fail(h, BV_EINVAL, "NULL argument");
   if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
@@ -738,6 +829,10 @@ static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
   BV_CUDA(h, cudaGraphLaunch(h->exec[h->h_theta->kind], h->stream));
   BV_CUDA(h, cudaStreamSynchronize(h->stream));
   const unsigned long long* acc = h->h_acc;
+  if (acc[6] != 0 && h->jitter) {
+    const bv_status js = jitter_retry(h, acc, loglik);
+    if (js != kJitterDefer) return js;
+  }
   if (acc[6] != 0) {
     unsigned long long mn = acc[7];
     if (h->world > 1) {
@@ -780,6 +875,18 @@ bv_status bv_loglik_host_y(bv_handle* h, const double* y, const double theta[3],
   BV_CUDA(h, cudaMemcpyAsync(h->d_y_stage, y, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
   BV_CUDA(h, bv::launch_scatter_y(h->d_y_stage, h->d_perm_of_id, h->n, h->d_pts, h->stream));
   return run_eval(h, theta, loglik);
+}
+
+bv_status bv_set_jitter(bv_handle* h, int32_t enable) {
+  if (!h) return BV_EINVAL;
+  h->jitter = enable != 0;
+  return BV_OK;
+}
+
+bv_status bv_jitter_events(const bv_handle* h, int64_t* events) {
+  if (!h || !events) return BV_EINVAL;
+  *events = h->jitter_events;
+  return BV_OK;
 }
 
 bv_status bv_owned_range(const bv_handle* h, int32_t* k_begin, int32_t* k_end) {

@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(NT) bv_block_v1_kernel(const PointRec* __restr
                                                          const int32_t* __restrict__ list,
                                                          const Theta* __restrict__ theta_dev,
                                                          double* __restrict__ out_u, double* __restrict__ out_d,
-                                                         unsigned long long* __restrict__ acc, int k_begin) {
+                                                         unsigned long long* __restrict__ acc, int k_begin,
+                                                         double jit) {
   extern __shared__ __align__(16) double smem[];
   const int q = list[blockIdx.x];
   const BlockDesc ds = desc[q];
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(NT) bv_block_v1_kernel(const PointRec* __restr
       double v;
       if (i < N) v = matern_from_d2(sqdist(P[i], pj), th);
       else v = pj.v;
+      if (i == j) v += jit;  // optional jitter retry: ε·σ² on the joint diagonal (reading G15b)
       cj[i - j] = v;
     }
   }
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(NT) bv_block_v1_kernel(const PointRec* __restr
       out_d[q] = logdet;
     } else {
       out_u[q] = 0.0;
-      out_d[q] = 0.0;
+      out_d[q] = failed_d();
     }
     accumulate_term(acc, c, st, k_begin + q);  // a9
   }
@@ -128,11 +130,11 @@ cudaError_t prepare_block_v1(int Nmax) {
 
 cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                             const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
-                            unsigned long long* acc, int k_begin) {
+                            unsigned long long* acc, int k_begin, double jit) {
   constexpr int NT = kV1Threads;
   const size_t smem = v1_smem_bytes(Nmax);
   if (nblocks == 0) return cudaSuccess;
-  bv_block_v1_kernel<NT><<<nblocks, NT, smem, s>>>(pts, nbr, desc, list, th, u, d, acc, k_begin);
+  bv_block_v1_kernel<NT><<<nblocks, NT, smem, s>>>(pts, nbr, desc, list, th, u, d, acc, k_begin, jit);
   return cudaGetLastError();
 }
 

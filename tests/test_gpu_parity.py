@@ -273,3 +273,48 @@ def test_classic_vecchia_kernel_equals_block_kernel(monkeypatch):
     sc = np.abs(ua) + np.abs(da) + 1.8378770664093456
     assert np.max(np.abs(da - db) / sc) <= 1e-12 and np.max(np.abs(ua - ub) / sc) <= 1e-12
     assert abs(la - lb) <= 1e-12 * abs(la)
+
+
+def _dup_plan_gpu(positions, n=400, bc=16, m=20, cfg=33):
+    p = bvgen.make_plan("c1", n=n, bc=bc, m=m, cfg=cfg)
+    locs = p.locs.copy()
+    y = bvgen.normal(4401, p.n)
+    for k in positions:  # a repeated location inside the block at position k
+        mem = np.where(p.block_id == p.order[k])[0]
+        locs[mem[1]] = locs[mem[0]]
+        y[mem[1]] = y[mem[0]] + 1e-6
+    return bvgen.Plan(locs, y, p.block_id, p.order, p.nbr_ptr, p.nbr_idx)
+
+
+@pytest.mark.parametrize("theta", [(1.0, 0.1, 0.5), (1.3, 0.12, 1.5), (0.7, 0.1, 0.83)])
+def test_jitter_mode_matches_oracle(theta):
+    """Optional jitter mode (reading G15b): the GPU retries exactly the oracle's blocks
+    with the same ε; jittered blocks agree to the conditioning the 1e-10 jitter leaves
+    (κ ≈ 1e10), all others to the usual FP64 bound; ℓ and jitter_events agree."""
+    q = _dup_plan_gpu((9, 4))
+    o = oracle.bv_loglik_jitter(q, theta)
+    assert o["events"] >= 2
+    bv = BlockVecchia(q)
+    with pytest.raises(NotPositiveDefinite):
+        bv.loglik(theta)  # mode off by default
+    assert bv.jitter_events == 0
+    bv.set_jitter(True)
+    ll, d, u = bv.loglik_terms(theta)
+    assert bv.jitter_events == o["events"]
+    l, _ = q.block_sizes()
+    scale = np.abs(o["u"]) + np.abs(o["d"]) + l * math.log(2 * math.pi)
+    err = np.maximum(np.abs(d - o["d"]), np.abs(u - o["u"])) / scale
+    jit = o["eps"] > 0
+    assert np.max(err[~jit]) <= 1e-10, np.max(err[~jit])
+    assert np.max(err[jit]) <= 1e-6, err[jit]
+    assert abs(ll - o["loglik"]) <= 1e-8 * abs(o["loglik"]), (ll, o["loglik"])
+    # an evaluation without failures resets the count and matches the mode-off result
+    p = bvgen.make_plan("c1", n=400, bc=16, m=20, cfg=33)
+    p = p.with_y(bvgen.normal(4402, p.n))
+    a, b = BlockVecchia(p), BlockVecchia(p)
+    b.set_jitter(True)
+    assert a.loglik(theta) == b.loglik(theta) and b.jitter_events == 0
+    bv.set_jitter(False)
+    with pytest.raises(NotPositiveDefinite) as e:
+        bv.loglik(theta)
+    assert e.value.failed_position == 4
