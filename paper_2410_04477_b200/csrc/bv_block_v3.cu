@@ -369,6 +369,12 @@ __device__ __forceinline__ double* slot_at(double* base, unsigned slot) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(base) + (slot << 9));
 }
 
+// A/B: split the GEMM accumulator chain when a warp has ≤ BV_GEMM_SPLIT tiles (0 = never).
+// Measured (gpurun_out/ab20): c4 214.5/214.1 evals/s at 2/5 vs 214.5 without; c5 m=30 no
+// change either: the late-panel DMMA chains are not the critical path.
+#ifndef BV_GEMM_SPLIT
+#define BV_GEMM_SPLIT 0
+#endif
 template <int NS, int MAXT>
 __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
                                        int uw, int lane) {
@@ -378,6 +384,31 @@ __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots
   const uint16_t* tI[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) tI[s] = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (kW - 1) * s) * TI;
+#if BV_GEMM_SPLIT
+  if constexpr (NS <= BV_GEMM_SPLIT) {
+    // few tiles per warp (late panels): the accumulator chain of 2J dependent DMMAs is
+    // the phase's latency; split it over the two k-halves (two independent chains)
+    double T[NS][2];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) T[s][0] = T[s][1] = 0.0;
+#pragma unroll 2
+    for (int K = 0; K < J; ++K) {
+      const double2 b = lds2(slot_at(sl, tJ[K]));
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        const double2 a = lds2(slot_at(sl, tI[s][K]));
+        dmma884(S[s][0], S[s][1], a.x, b.x);
+        dmma884(T[s][0], T[s][1], a.y, b.y);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      S[s][0] += T[s][0];
+      S[s][1] += T[s][1];
+    }
+    return;
+  }
+#endif
 #pragma unroll 2
   for (int K = 0; K < J; ++K) {
     const double2 b = lds2(slot_at(sl, tJ[K]));
@@ -391,6 +422,10 @@ __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots
 }
 
 
+// Half-tiles of generation in flight per update warp.  Measured (gpurun_out/ab20):
+// 2 → 213.7/215.2 evals/s at c4 vs 214.0/214.9 at 1 (noise); kept at 1.
+// (Same run: BV_TRSM_U=0, row-substitution panel solves on the update warps,
+// 197.8/199.2 — the DMMA + refinement solve stays.)
 #ifndef BV_V3_GEN_UNROLL
 #define BV_V3_GEN_UNROLL 1
 #endif
