@@ -156,10 +156,23 @@ struct Layout {
   }
 };
 
+// KIND kPre: the general-ν Σ entries were written by the pre-generation kernel
+// (bv_pregen_kernel below) as each block's packed lower triangle, pre[r(r+1)/2 + c],
+// r ≥ c, r < N; the block kernel reads instead of evaluating K_ν.  Same function,
+// same arguments → bitwise the entries the in-kernel path computes (incl. the
+// padding: 0 off the diagonal, σ² on it, as Eq. (7) gives for the far points).
+constexpr int kPre = 4;
+__device__ __forceinline__ double pre_entry(const double* __restrict__ pre, int r, int c, int N, double s2) {
+  const int rr = r > c ? r : c, cc = r > c ? c : r;
+  return rr < N ? pre[(rr * (rr + 1) >> 1) + cc] : (rr == cc ? s2 : 0.0);
+}
+
 template <int KIND>
 __device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec& pc, int r, int c, int N,
-                                             const Theta& th, const double* tab64) {
-  const double v = matern_kind<KIND>(sqdist(pr, pc), th, tab64);
+                                             const Theta& th, const double* tab64, const double* pre) {
+  double v;
+  if constexpr (KIND == kPre) v = pre_entry(pre, r, c, N, th.sigma2);
+  else v = matern_kind<KIND>(sqdist(pr, pc), th, tab64);
   return (r == N) ? pc.v : v;  // the y row; padding entries are 0 by construction (far points)
 }
 
@@ -460,7 +473,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
                    const Theta* __restrict__ theta_dev, const int16_t* __restrict__ tabs,
                    const int32_t* __restrict__ tab_off, const double* __restrict__ exp_tab, int TImax, int cap,
                    double* __restrict__ out_u, double* __restrict__ out_d, unsigned long long* __restrict__ acc,
-                   int k_begin, double* __restrict__ gslots, int nblocks) {
+                   int k_begin, double* __restrict__ gslots, int nblocks, const double* __restrict__ pre,
+                   const int64_t* __restrict__ pre_off) {
   constexpr bool GS = MAXT >= kGsMaxT;
   extern __shared__ __align__(16) double smem[];
   const Layout Ly(TImax, GS ? 0 : cap);
@@ -468,6 +482,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   const int q = list[bidx];
   const BlockDesc ds = desc[q];
   const int m = ds.m, l = ds.l, N = m + l;
+  const double* preb = KIND == kPre ? pre + pre_off[q] : nullptr;
   const int TJ = (N + 7) >> 3;  // column panels
   const int TI = (N + 8) >> 3;  // tile rows (incl. the y row)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -521,7 +536,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
 #pragma unroll 2
   for (int e = tid; e < TI * 64; e += kNT) {
     const int I = e >> 6, r = 8 * I + ((e >> 3) & 7), c = e & 7;
-    const double v = joint_entry<KIND>(P[r], P[c], r, c, N, th, etab);
+    const double v = joint_entry<KIND>(P[r], P[c], r, c, N, th, etab, preb);
     if (I == 0) dtile[e] = v;
     else slots[64 * tab[I * TI] + (e & 63)] = v;
   }
@@ -651,7 +666,9 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
 #pragma unroll(kV3GenUnroll)
           for (int h = uw - 1; h < nh; h += kW - 1) {
             const int I = J + 1 + (h >> 1), r = r0 + 4 * h;
-            double v = matern_kind<KIND>(sqdist(P[r], pc), th, etab);
+            double v;
+            if constexpr (KIND == kPre) v = pre_entry(preb, r, c, N, th.sigma2);
+            else v = matern_kind<KIND>(sqdist(P[r], pc), th, etab);
             v = (r == N) ? pc.v : v;  // padding entries are 0 by construction (far points)
             double* dst = (h < 2) ? ptile : slot_at(slots, tabu[I * TI + J + 1]);
             dst[32 * (h & 1) + lane] = v;
@@ -833,11 +850,12 @@ size_t v3_smem_bytes(int TImax, int cap) {
 template <int MAXT>
 static cudaError_t v3_prep(size_t smem) {
   cudaError_t e = cudaSuccess;
-  for (int k = 0; k < 4 && e == cudaSuccess; ++k) {
+  for (int k = 0; k < 5 && e == cudaSuccess; ++k) {
     const void* f = k == 0 ? (const void*)v3::bv_block_v3_kernel<MAXT, 0>
                   : k == 1 ? (const void*)v3::bv_block_v3_kernel<MAXT, 1>
                   : k == 2 ? (const void*)v3::bv_block_v3_kernel<MAXT, 2>
-                           : (const void*)v3::bv_block_v3_kernel<MAXT, 3>;
+                  : k == 3 ? (const void*)v3::bv_block_v3_kernel<MAXT, 3>
+                           : (const void*)v3::bv_block_v3_kernel<MAXT, v3::kPre>;
     e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   return e;
@@ -863,15 +881,18 @@ template <int MAXT>
 static void v3_launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, const PointRec* pts,
                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                            const int16_t* tabs, const int32_t* tab_off, const double* etab, int TImax, int cap,
-                           double* u, double* d, unsigned long long* acc, int k_begin, double* gslots, int grid) {
+                           double* u, double* d, unsigned long long* acc, int k_begin, double* gslots, int grid,
+                           const double* pre, const int64_t* pre_off) {
 #define BV_K(KD)                                                                                             \
   v3::bv_block_v3_kernel<MAXT, KD><<<grid, v3::kNT, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, \
-                                                               TImax, cap, u, d, acc, k_begin, gslots, nblocks)
+                                                               TImax, cap, u, d, acc, k_begin, gslots, nblocks, \
+                                                               pre, pre_off)
   switch (kind) {
     case 0: BV_K(0); break;
     case 1: BV_K(1); break;
     case 2: BV_K(2); break;
-    default: BV_K(3); break;
+    case 3: BV_K(3); break;
+    default: BV_K(v3::kPre); break;
   }
 #undef BV_K
 }
@@ -879,7 +900,8 @@ static void v3_launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, c
 cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid) {
+                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid, const double* pre,
+                            const int64_t* pre_off) {
   if (nblocks == 0) return cudaSuccess;
   const size_t smem = v3_smem_bytes(TImax, cap);
   const int grid = v3_global_slots(TImax) ? (nblocks < gs_grid ? nblocks : gs_grid) : nblocks;
@@ -887,12 +909,57 @@ cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStrea
 #define BV_MT(MT)                                                                                          \
   case MT:                                                                                                 \
     v3_launch_kind<MT>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, \
-                       acc, k_begin, gslots, grid);                                                        \
+                       acc, k_begin, gslots, grid, pre, pre_off);                                          \
     break;
     BV_MT(1) BV_MT(2) BV_MT(3) BV_MT(4) BV_MT(5) BV_MT(6) BV_MT(8) BV_MT(10) BV_MT(12) BV_MT(16) BV_MT(20)
 #undef BV_MT
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ general-ν pre-generation
+// a3 for small plans with general ν (c2: 500 blocks, fewer than one wave of
+// block-kernel CTAs, K_ν costs hundreds of FP64 instructions per entry): one
+// kernel evaluates every block's packed lower triangle of Σ with all SMs' warps
+// into an L2-resident buffer, then the block kernel (KIND kPre) only reads it.
+namespace v3 {
+constexpr int kPgThreads = 256;
+template <int KIND>
+__global__ void __launch_bounds__(kPgThreads) bv_pregen_kernel(const PointRec* __restrict__ pts,
+                                                              const int32_t* __restrict__ nbr,
+                                                              const BlockDesc* __restrict__ desc,
+                                                              const Theta* __restrict__ theta_dev,
+                                                              const double* __restrict__ exp_tab,
+                                                              const int64_t* __restrict__ pre_off,
+                                                              double* __restrict__ pre) {
+  __shared__ double etab[64];
+  if (threadIdx.x < 64) etab[threadIdx.x] = exp_tab[threadIdx.x];
+  __syncthreads();
+  const Theta th = *theta_dev;
+  const int q = blockIdx.x;
+  const BlockDesc ds = desc[q];
+  const int m = ds.m, N = ds.m + ds.l;
+  const int E = N * (N + 1) / 2;
+  double* out = pre + pre_off[q];
+  for (int e = blockIdx.y * kPgThreads + threadIdx.x; e < E; e += kPgThreads * gridDim.y) {
+    int r = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);  // row of packed index e (fixed up exactly)
+    while ((r * (r + 1) >> 1) > e) --r;
+    while (((r + 1) * (r + 2) >> 1) <= e) ++r;
+    const int c = e - (r * (r + 1) >> 1);
+    const PointRec pr = pts[(r < m) ? nbr[ds.nbr_off + r] : ds.pstart + (r - m)];
+    const PointRec pc = pts[(c < m) ? nbr[ds.nbr_off + c] : ds.pstart + (c - m)];
+    out[e] = matern_kind<KIND>(sqdist(pr, pc), th, etab);
+  }
+}
+}  // namespace v3
+
+cudaError_t launch_pregen(int nblocks, int chunks, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
+                          const BlockDesc* desc, const Theta* th, const double* etab, const int64_t* pre_off,
+                          double* pre) {
+  if (nblocks == 0) return cudaSuccess;
+  v3::bv_pregen_kernel<kNuGeneral><<<dim3(nblocks, chunks), v3::kPgThreads, 0, s>>>(pts, nbr, desc, th, etab,
+                                                                                      pre_off, pre);
   return cudaGetLastError();
 }
 

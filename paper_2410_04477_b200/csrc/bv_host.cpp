@@ -46,7 +46,11 @@ cudaError_t prepare_block_v3(size_t max_smem);
 cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid);
+                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid,
+                            const double* pre = nullptr, const int64_t* pre_off = nullptr);
+cudaError_t launch_pregen(int nblocks, int chunks, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
+                          const BlockDesc* desc, const Theta* th, const double* etab, const int64_t* pre_off,
+                          double* pre);
 bool v3_global_slots(int TI);
 int debug_phase_cycles(unsigned long long* out, int reset);
 int debug_v3_cycles(unsigned long long* out, int reset);
@@ -181,6 +185,10 @@ struct bv_handle {
   int32_t* d_jlist = nullptr;                // failed positions being retried
   unsigned long long* d_jacc = nullptr;      // the retry's own accumulator (kAccSlots) + 3 allreduce slots
   int v1_ready = 0;                          // largest N prepare_block_v1 was called for
+  // general-ν pre-generation (small plans): packed Σ triangles, offsets per local position
+  double* d_pre = nullptr;
+  int64_t* d_pre_off = nullptr;
+  int pre_chunks = 0;
 };
 
 namespace {
@@ -299,7 +307,7 @@ void release(bv_handle* h) {
   }
   if (h->comm) ncclCommDestroy(h->comm);
   void* dev[] = {h->d_gslots, h->d_pts, h->d_nbr, h->d_desc, h->d_list, h->d_theta, h->d_u, h->d_d,
-                 h->d_jlist, h->d_jacc, h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
+                 h->d_jlist, h->d_jacc, h->d_pre, h->d_pre_off, h->d_acc, h->d_min, h->d_perm_of_id, h->d_y_stage, h->d_tabs, h->d_tab_off, h->d_exptab};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (h->h_theta) cudaFreeHost(h->h_theta);
@@ -633,6 +641,21 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   TRY(upload(h, &h->d_desc, desc.data(), desc.size()));
   h->h_N.resize((size_t)h->nq);
   for (int32_t q = 0; q < h->nq; ++q) h->h_N[q] = Nq(q);
+  {
+    // General-ν pre-generation (bv_block_v3.cu, bv_pregen_kernel): when every block's
+    // packed Σ fits a small L2-resident buffer (≤ 64 MB: c1, c2), the K_ν entries are
+    // evaluated by one all-SM kernel instead of by the block kernel's update warps.
+    // BV_NO_PREGEN=1 disables it (A/B and the bitwise-equality test).
+    const char* npg = std::getenv("BV_NO_PREGEN");
+    std::vector<int64_t> off((size_t)h->nq + 1, 0);
+    for (int32_t q = 0; q < h->nq; ++q) off[(size_t)q + 1] = off[q] + (int64_t)Nq(q) * (Nq(q) + 1) / 2;
+    constexpr int64_t kPreMaxBytes = 64ll << 20;
+    if (!use_v1 && !use_v2 && !(npg && npg[0] == '1') && h->nq > 0 && off[(size_t)h->nq] * 8 <= kPreMaxBytes) {
+      TRY(upload<double>(h, &h->d_pre, nullptr, (size_t)std::max<int64_t>(1, off[(size_t)h->nq])));
+      TRY(upload(h, &h->d_pre_off, off.data(), (size_t)h->nq));
+      h->pre_chunks = std::max(1, std::min(64, (16 * 148 + h->nq - 1) / h->nq));
+    }
+  }
   TRY(upload(h, &h->d_list, list.data(), list.size()));
   TRY(upload(h, &h->d_perm_of_id, perm_of_id.data(), perm_of_id.size()));
   h->h_perm_of_id = perm_of_id;
@@ -686,6 +709,10 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     if (e == cudaSuccess) e = cudaMemsetAsync(h->d_acc, 0, sizeof(unsigned long long) * 7, h->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(h->d_acc + 7, 0xff, sizeof(unsigned long long), h->stream);
     if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k0, h->stream, cudaEventRecordExternal);
+    const bool pre = kind == bv::kNuGeneral && h->d_pre != nullptr;
+    if (e == cudaSuccess && pre)
+      e = bv::launch_pregen(h->nq, h->pre_chunks, h->stream, h->d_pts, h->d_nbr, h->d_desc, h->d_theta, h->d_exptab,
+                            h->d_pre_off, h->d_pre);
     if (e == cudaSuccess) e = cudaEventRecord(h->fork_ev, h->stream);
     const int nbr_streams = std::min<int>(bv_handle::kBranches, std::max<int>(1, (int)h->buckets.size()));
     for (int b = 0; b < nbr_streams && e == cudaSuccess; ++b) e = cudaStreamWaitEvent(h->side[b], h->fork_ev, 0);
@@ -703,10 +730,10 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
         e = bv::launch_cv(kind, b.count, st, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset, h->d_theta,
                           h->d_exptab, h->d_u, h->d_d, h->d_acc, h->kb);
       else
-        e = bv::launch_block_v3(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
+        e = bv::launch_block_v3(pre ? 4 : kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
                                 h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
                                 h->d_d, h->d_acc, h->kb, h->d_gslots ? h->d_gslots + b.gs_off : nullptr,
-                                h->gs_grid);
+                                h->gs_grid, h->d_pre, h->d_pre_off);
     }
     for (int b = 0; b < nbr_streams && e == cudaSuccess; ++b) {
       e = cudaEventRecord(h->join_ev[b], h->side[b]);

@@ -318,3 +318,22 @@ def test_jitter_mode_matches_oracle(theta):
     with pytest.raises(NotPositiveDefinite) as e:
         bv.loglik(theta)
     assert e.value.failed_position == 4
+
+
+@pytest.mark.parametrize("shape", [dict(n=2000, bc=20, m=30, cfg=51), dict(n=6000, bc=150, m=60, cfg=52)])
+def test_general_nu_pregeneration_is_bitwise_equal(shape, monkeypatch):
+    """General ν on small plans: the all-SM pre-generation kernel + block kernel (KIND kPre)
+    gives bitwise the ℓ, d_k, u_k of the in-kernel K_ν path (BV_NO_PREGEN=1): same
+    function, same arguments, same order of the elimination."""
+    theta = (1.1, 0.06, 0.83)
+    p = bvgen.make_plan("c1", **shape)
+    p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(5101, p.n)))
+    a = BlockVecchia(p)
+    monkeypatch.setenv("BV_NO_PREGEN", "1")
+    b = BlockVecchia(p)
+    assert a.launches_per_eval == b.launches_per_eval
+    la, da, ua = a.loglik_terms(theta)
+    lb, db, ub = b.loglik_terms(theta)
+    assert la == lb and np.array_equal(da, db) and np.array_equal(ua, ub)
+    o = oracle.bv_loglik(p, theta)
+    assert abs(la - o["loglik"]) <= 1e-9 * abs(o["loglik"])
