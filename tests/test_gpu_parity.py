@@ -337,3 +337,33 @@ def test_general_nu_pregeneration_is_bitwise_equal(shape, monkeypatch):
     assert la == lb and np.array_equal(da, db) and np.array_equal(ua, ub)
     o = oracle.bv_loglik(p, theta)
     assert abs(la - o["loglik"]) <= 1e-9 * abs(o["loglik"])
+
+
+def test_jitter_mode_classic_vecchia_positions():
+    """bc = n: a position whose point repeats its first neighbour fails in the warp kernel
+    (bv_cv.cu, d_k = NaN marker) and is retried like any block (reading G15b)."""
+    theta = (1.0, 0.078809, 1.5)
+    n = 800
+    p = bvgen.make_plan("c1", n=n, bc=n, m=25, cfg=38)
+    pt = np.empty(n, dtype=np.int32)
+    pt[p.block_id] = np.arange(n, dtype=np.int32)
+    locs, y = p.locs.copy(), bvgen.normal(3803, n)
+    for k in (300, 650):
+        i = p.nbr_idx[p.nbr_ptr[k]]
+        locs[pt[p.order[k]]] = locs[i]
+        y[pt[p.order[k]]] = y[i] + 1e-6
+    q = bvgen.Plan(locs, y, p.block_id, p.order, p.nbr_ptr, p.nbr_idx)
+    o = oracle.bv_loglik_jitter(q, theta)
+    assert o["events"] >= 2
+    bv = BlockVecchia(q)
+    with pytest.raises(NotPositiveDefinite) as e:
+        bv.loglik(theta)
+    assert e.value.failed_position == 300
+    bv.set_jitter(True)
+    ll, d, u = bv.loglik_terms(theta)
+    assert bv.jitter_events == o["events"]
+    scale = np.abs(o["u"]) + np.abs(o["d"]) + math.log(2 * math.pi)
+    err = np.maximum(np.abs(d - o["d"]), np.abs(u - o["u"])) / scale
+    jit = o["eps"] > 0
+    assert np.max(err[~jit]) <= 1e-10 and np.max(err[jit]) <= 1e-6
+    assert abs(ll - o["loglik"]) <= 1e-8 * abs(o["loglik"])
