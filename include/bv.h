@@ -207,8 +207,9 @@ void* bv_stream(const bv_handle* h);
  * recent evaluation, from CUDA events captured inside the graph. */
 bv_status bv_last_kernel_ms(const bv_handle* h, float* ms);
 
-/* Kernel launches per evaluation on this rank (for the bench's gpu_launches);
- * a general-ν evaluation of a small plan (Σ ≤ 64 MB) adds one pre-generation launch. */
+/* Kernel launches per evaluation on this rank (for the bench's gpu_launches), for
+ * the Matérn kind of the most recent evaluation: after a general-ν evaluation of
+ * a small plan (Σ ≤ 64 MB) it includes the one pre-generation launch. */
 int32_t bv_launches_per_eval(const bv_handle* h);
 
 /* Free everything the handle owns.  NULL is a no-op. */

@@ -218,7 +218,11 @@ class BlockVecchia:
         kb, ke = C.c_int32(), C.c_int32()
         L.bv_owned_range(self._h, C.byref(kb), C.byref(ke))
         self.k_begin, self.k_end = kb.value, ke.value
-        self.launches_per_eval = L.bv_launches_per_eval(self._h)
+
+    @property
+    def launches_per_eval(self) -> int:
+        """Kernels per evaluation for the Matérn kind of the latest evaluation."""
+        return int(self._L.bv_launches_per_eval(self._h))
 
     def _check(self, st):
         if st == BV_OK:

@@ -189,6 +189,7 @@ struct bv_handle {
   double* d_pre = nullptr;
   int64_t* d_pre_off = nullptr;
   int pre_chunks = 0;
+  int last_kind = -1;  // MaternKind of the most recent evaluation
 };
 
 namespace {
@@ -853,6 +854,7 @@ static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
   if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
   BV_CUDA(h, cudaSetDevice(h->device));
   fill_theta_buf(h->h_theta, h->d_theta, theta);
+  h->last_kind = h->h_theta->kind;
   BV_CUDA(h, cudaGraphLaunch(h->exec[h->h_theta->kind], h->stream));
   BV_CUDA(h, cudaStreamSynchronize(h->stream));
   const unsigned long long* acc = h->h_acc;
@@ -951,6 +953,7 @@ int32_t bv_launches_per_eval(const bv_handle* h) {
   int32_t c = 0;  // one kernel per non-empty bucket (the reduction is fused into them)
   for (const Bucket& b : h->buckets)
     if (b.count > 0) ++c;
+  if (h->last_kind == bv::kNuGeneral && h->d_pre) ++c;  // the general-ν pre-generation kernel
   return c;
 }
 
