@@ -289,11 +289,12 @@ def run_predict(args):
     for _ in range(max(1, args.warmup)):
         bv.predict(theta, pp)
     torch.cuda.synchronize()
-    ts = []
+    ts, kms = [], []
     for _ in range(args.steps):
         t = time.perf_counter()
         bv.predict(theta, pp, want_cov=True)
         ts.append(time.perf_counter() - t)
+        kms.append(bv.last_kernel_ms())  # events around the prediction kernel alone
     bv.close()
     lsz = np.bincount(pp.block_id, minlength=bc_new)
     N = (lsz + plan.m).astype(np.float64)
@@ -305,7 +306,10 @@ def run_predict(args):
            "config": {"workload": f"{args.config} prediction: n*={n_new:,} new points, bc*={bc_new:,} blocks, "
                                   f"m={plan.m}, theta={theta}", "n_train": plan.n, "n_new": n_new, "bc_new": bc_new,
                       "m": plan.m, "max_joint": int(N.max())},
-           "fp64_tflops": flops / sec / 1e12, "note": "wall time of bv_predict incl. host-side plan marshalling"}
+           "fp64_tflops": flops / sec / 1e12, "note": "wall time of bv_predict incl. host-side plan marshalling",
+           "kernel": {"ms": float(np.median(kms)), "points_per_s": n_new / (float(np.median(kms)) / 1e3),
+                      "fp64_tflops": flops / (float(np.median(kms)) / 1e3) / 1e12,
+                      "what": "CUDA events around the prediction kernel (bv_last_kernel_ms after bv_predict)"}}
     print(json.dumps(out))
     return 0
 

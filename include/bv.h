@@ -204,7 +204,8 @@ void* bv_stream(const bv_handle* h);
 
 /* Device time (ms) of the block kernels (all size buckets, gather through
  * per-block terms; excludes θ upload, reduction and allreduce) in the most
- * recent evaluation, from CUDA events captured inside the graph. */
+ * recent evaluation, from CUDA events captured inside the graph.  After a
+ * bv_predict it is the device time of the prediction kernel instead. */
 bv_status bv_last_kernel_ms(const bv_handle* h, float* ms);
 
 /* Kernel launches per evaluation on this rank (for the bench's gpu_launches), for

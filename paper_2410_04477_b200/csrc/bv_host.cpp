@@ -190,6 +190,8 @@ struct bv_handle {
   int64_t* d_pre_off = nullptr;
   int pre_chunks = 0;
   int last_kind = -1;  // MaternKind of the most recent evaluation
+  std::vector<int64_t> pred_stamp;  // bv_predict's duplicate-neighbour table (n entries)
+  int64_t pred_epoch = 0;
 };
 
 namespace {
@@ -999,13 +1001,19 @@ bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp
   constexpr int kPredNmax = 235;  // predict_smem_bytes(235) ≤ 232448
   size_t smax = 0;
   {
-    std::vector<int32_t> stamp((size_t)h->n, -1);
+    // duplicate check: h->pred_stamp[id] holds the last (call epoch, block) that used id, so the
+    // n-sized table is allocated once per handle instead of once per call
+    if (h->pred_stamp.size() != (size_t)h->n) h->pred_stamp.assign((size_t)h->n, -1);
+    std::vector<int64_t>& stamp = h->pred_stamp;
+    const int64_t base = h->pred_epoch;
+    h->pred_epoch += bc;
     for (int32_t b = 0; b < bc; ++b) {
       for (int64_t q = pp->nbr_ptr[b]; q < pp->nbr_ptr[b + 1]; ++q) {
         const int32_t id = pp->nbr_idx[q];
         if (id < 0 || id >= h->n) return fail(h, BV_EINVAL, "nbr_idx[" + std::to_string(q) + "] out of range");
-        if (stamp[id] == b) return fail(h, BV_EINVAL, "duplicate neighbour in prediction block " + std::to_string(b));
-        stamp[id] = b;
+        if (stamp[id] == base + b)
+          return fail(h, BV_EINVAL, "duplicate neighbour in prediction block " + std::to_string(b));
+        stamp[id] = base + b;
       }
       const int N = (int)(pp->nbr_ptr[b + 1] - pp->nbr_ptr[b] + bptr[(size_t)b + 1] - bptr[b]);
       if (N > kPredNmax)
@@ -1078,8 +1086,10 @@ bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp
   fill_theta_buf(h->h_theta, h->d_theta, theta);
   PCALL(cudaMemcpyAsync(h->d_theta, h->h_theta, sizeof(bv::Theta) * bv::kThetaSlots, cudaMemcpyHostToDevice, st));
   PCALL(bv::prepare_predict(std::max<size_t>(smax, 1024)));
+  PCALL(cudaEventRecord(h->ev_k0, st));  // bv_last_kernel_ms then reports the prediction kernel
   PCALL(bv::launch_predict(bc, smax, st, h->d_pts, d_np, d_nbr, d_desc, h->d_theta, d_coff, d_mean, d_var, d_cov,
                            d_status));
+  PCALL(cudaEventRecord(h->ev_k1, st));
   std::vector<double> hm((size_t)nn), hv((size_t)nn);
   std::vector<int32_t> hs((size_t)bc);
   PCALL(cudaMemcpyAsync(hm.data(), d_mean, sizeof(double) * nn, cudaMemcpyDeviceToHost, st));

@@ -16,7 +16,9 @@
 // "for conditional simulations", l.15; PAPER.md:242 takes its diagonal).
 //
 // Not the likelihood hot path (the paper predicts once per fit): one column
-// per elimination step, all threads on the trailing update, packed columns as
+// per elimination step, all 16 warps on the trailing update (512 threads, two
+// CTAs per SM: the step is latency-bound, 512 beat 256 threads by 15 % at c4
+// and a register-cached column j did not help), packed columns as
 // in bv_kernels.cu's v1 kernel.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -31,9 +33,9 @@ namespace {
 __device__ __forceinline__ int pk_off(int j, int Na) { return j * Na - (j * (j - 1)) / 2; }
 }  // namespace
 
-constexpr int kPredNT = 256;
+constexpr int kPredNT = 512;
 
-__global__ void __launch_bounds__(kPredNT) bv_predict_kernel(const PointRec* __restrict__ train,
+__global__ void __launch_bounds__(kPredNT, 2) bv_predict_kernel(const PointRec* __restrict__ train,
                                                              const PointRec* __restrict__ newp,
                                                              const int32_t* __restrict__ nbr,
                                                              const BlockDesc* __restrict__ desc,

@@ -147,4 +147,14 @@ def test_predict_gpu_rejects_bad_plans():
     big = bvgen.make_pred_plan(p.locs, pp.locs_new, 1, 200)  # m + l = 300 > 235
     with pytest.raises(BVError):
         bv.predict((1.0, 0.078809, 0.5), big)
+    # the handle's duplicate-neighbour table persists across calls: repeated predictions agree
+    # bitwise, and a duplicate is still caught after successful calls
+    m1, v1 = bv.predict((1.0, 0.078809, 0.5), pp)
+    assert bv.last_kernel_ms() > 0.0
+    m2, v2 = bv.predict((1.0, 0.078809, 0.5), pp)
+    assert np.array_equal(m1, m2) and np.array_equal(v1, v2)
+    dup = bvgen.PredPlan(pp.locs_new, pp.block_id, pp.nbr_ptr, pp.nbr_idx.copy())
+    dup.nbr_idx[1] = dup.nbr_idx[0]
+    with pytest.raises(BVError):
+        bv.predict((1.0, 0.078809, 0.5), dup)
     bv.close()
