@@ -15,10 +15,11 @@
 // HBM, and no second factorisation is needed (the paper returns Σ_B* itself,
 // "for conditional simulations", l.15; PAPER.md:242 takes its diagonal).
 //
-// Not the likelihood hot path (the paper predicts once per fit): one column
-// per elimination step, all 16 warps on the trailing update (512 threads, two
-// CTAs per SM: the step is latency-bound, 512 beat 256 threads by 15 % at c4
-// and a register-cached column j did not help), packed columns as
+// Not the likelihood hot path (the paper predicts once per fit): two columns
+// per pass over the trailing matrix (bitwise the same as two rank-1 steps),
+// all 16 warps on the trailing update (512 threads, two CTAs per SM: the pass
+// is latency-bound; at c4 512 threads beat 256 by 15 %, the two-column pass
+// another 1.45x, a register-cached column j did not help), packed columns as
 // in bv_kernels.cu's v1 kernel.
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kPredNT, 2) bv_predict_kernel(const PointRec* 
   __syncthreads();
   // Σcon⁻¹ applied by eliminating the first m columns (l.10-11)
   int fail = 0;
-  for (int j = 0; j < m; ++j) {
+  for (int j = 0; j < m; j += 2) {
     const double* cj = A + pk_off(j, Na);
     const double p = cj[0];
     if (!(p > kPivotFloor * th.sigma2) || !isfinite(p)) {  // uniform across the CTA (reading G15)
@@ -81,11 +82,39 @@ __global__ void __launch_bounds__(kPredNT, 2) bv_predict_kernel(const PointRec* 
       break;
     }
     const double inv = 1.0 / p;
-    // trailing update, one warp per column k = j+1..N−1 (rows k..N, the appended row included)
-    for (int k = j + 1 + (tid >> 5); k < N; k += kPredNT / 32) {
+    if (j + 1 == m) {  // last (odd) column: one rank-1 step
+      // trailing update, one warp per column k = j+1..N−1 (rows k..N, the appended row included)
+      for (int k = j + 1 + (tid >> 5); k < N; k += kPredNT / 32) {
+        double* ck = A + pk_off(k, Na);
+        const double w = cj[k - j] * inv;
+        for (int i = k + (tid & 31); i <= N; i += 32) ck[i - k] = fma(-cj[i - j], w, ck[i - k]);
+      }
+      __syncthreads();
+      break;
+    }
+    // two columns per pass over the trailing matrix: column j+1 first takes step j's update,
+    // then every later column takes step j's and step j+1's FMAs back to back — the same
+    // operations in the same order as two rank-1 steps, so the result is bitwise identical
+    double* c1 = A + pk_off(j + 1, Na);
+    {
+      const double w = cj[1] * inv;
+      for (int i = j + 1 + tid; i <= N; i += kPredNT) c1[i - j - 1] = fma(-cj[i - j], w, c1[i - j - 1]);
+    }
+    __syncthreads();
+    const double p1 = c1[0];
+    if (!(p1 > kPivotFloor * th.sigma2) || !isfinite(p1)) {
+      fail = 1;
+      break;
+    }
+    const double inv1 = 1.0 / p1;
+    for (int k = j + 2 + (tid >> 5); k < N; k += kPredNT / 32) {
       double* ck = A + pk_off(k, Na);
-      const double w = cj[k - j] * inv;
-      for (int i = k + (tid & 31); i <= N; i += 32) ck[i - k] = fma(-cj[i - j], w, ck[i - k]);
+      const double w0 = cj[k - j] * inv;
+      const double w1 = c1[k - j - 1] * inv1;
+      for (int i = k + (tid & 31); i <= N; i += 32) {
+        const double x = fma(-cj[i - j], w0, ck[i - k]);
+        ck[i - k] = fma(-c1[i - j - 1], w1, x);
+      }
     }
     __syncthreads();
   }

@@ -120,6 +120,8 @@ def gpu_case(name, theta, n_new, bc_new, m, cfg):
     ("c1", (1.0, 0.078809, 1.5), 500, 20, 120),
     ("c2", (1.0, 0.052537, 1.5), 2000, 200, 60),
     ("c2", (0.9, 0.06, 1.31), 1000, 100, 60),
+    ("c1", (1.0, 0.078809, 1.5), 300, 30, 31),  # odd m: the kernel's single-column tail step
+    ("c1", (1.0, 0.078809, 2.5), 200, 20, 1),
 ])
 def test_predict_gpu_parity(name, theta, n_new, bc_new, m):
     from paper_2410_04477_b200 import BlockVecchia
