@@ -19,7 +19,8 @@
 // per pass over the trailing matrix (bitwise the same as two rank-1 steps),
 // all 16 warps on the trailing update (512 threads, two CTAs per SM: the pass
 // is latency-bound; at c4 512 threads beat 256 by 15 %, the two-column pass
-// another 1.45x, a register-cached column j did not help), packed columns as
+// another 1.45x; a register-cached column j and a generic 4-column panel
+// (2.61 ms vs 2.31) did not help), packed columns as
 // in bv_kernels.cu's v1 kernel.
 #include <cuda_runtime.h>
 #include <stdint.h>
