@@ -95,9 +95,22 @@ bv_status bv_nccl_unique_id(void* out128);
  * (PAPER.md:411). */
 bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out);
 
-/* ℓ(θ) for θ = (σ², β, ν) (host array of 3 doubles, each finite and > 0).
- * Closed forms are used when ν is exactly 0.5, 1.5 or 2.5; any other ν takes
- * the general K_ν path.  Collective when world > 1 (all ranks, identical θ).
+/* TEST-ONLY rank emulation (no communicator).  Builds exactly the device layout
+ * rank `rank` of `world` would get from bv_setup (the same contiguous,
+ * cost-balanced position range, rank-local neighbour slice and rebased
+ * offsets — DESIGN.md §6, "independent of each other"), but
+ * creates no NCCL communicator and reduces nothing across ranks: bv_loglik on
+ * such a handle returns this rank's PARTIAL sum, and bv_loglik_acc its exact
+ * fixed-point accumulator, so the G partial accumulators can be summed by the
+ * caller and compared with the single-rank one.  Lets one GPU evaluate the
+ * ranks of a world > 1 partition one after another (no rank waits on another).
+ * Failing positions are reported as GLOBAL permuted positions k.  Errors as
+ * bv_setup. */
+bv_status bv_setup_rank_local(const bv_plan* plan, int32_t device, int32_t rank, int32_t world, bv_handle** out);
+
+/* ℓ(θ) for θ = (σ², β, ν) (host array of 3 doubles): σ², β finite and > 0;
+ * ν exactly 0.5, 1.5 or 2.5 (closed forms) or any ν in [0.2, 3] (the general
+ * K_ν path, validated on that range; the MLE box of SURVEY §8d).  Collective when world > 1 (all ranks, identical θ).
  * Errors: BV_EINVAL (bad θ), BV_ENOTPD (*loglik = -INFINITY), BV_ECUDA,
  * BV_ENCCL. */
 bv_status bv_loglik(bv_handle* h, const double theta[3], double* loglik);
@@ -108,6 +121,15 @@ bv_status bv_loglik(bv_handle* h, const double theta[3], double* loglik);
  * (host arrays of k_end - k_begin doubles; either may be NULL). */
 bv_status bv_loglik_terms(bv_handle* h, const double theta[3], double* loglik, double* logdet, double* quad);
 
+/* One evaluation, returning the exact fixed-point accumulator instead of ℓ:
+ * acc_out[0..5] = the six 32-bit chunk sums of round(t_k·2⁶⁴) (
+ * ℓ = bv_fixed_decode(acc_out)), acc_out[6] = failed-block count,
+ * acc_out[7] = (smallest failing global position << 8 | status) or UINT64_MAX.
+ * After a world > 1 bv_setup the chunks are already all-reduced; after
+ * bv_setup_rank_local they are this rank's partial.  Returns BV_OK or
+ * BV_ENOTPD like bv_loglik (acc_out is filled either way), or an error. */
+bv_status bv_loglik_acc(bv_handle* h, const double theta[3], uint64_t acc_out[8]);
+
 /* Optional jitter mode (off by default; reading G15b, SPEC.md:197,
  * :238).  When enabled, a bv_loglik* evaluation in which some block is not
  * positive definite recomputes each failed block with ε·σ² added to every
@@ -115,8 +137,9 @@ bv_status bv_loglik_terms(bv_handle* h, const double theta[3], double* loglik, d
  * ε = 1e-10, 1e-8, 1e-6 in turn, keeping the first that succeeds; only if
  * one still fails does the call return BV_ENOTPD.  The retry runs off the
  * captured graph and only after a failure, so evaluations without failures
- * cost the same.  Blocks with joint size > 235 are not retried.  Collective
- * when world > 1: set it identically on every rank.  Errors: BV_EINVAL (NULL). */
+ * cost the same.  Every joint size the evaluation supports is retried, with
+ * the same kernels and ε·σ² added to the diagonal inside the factorisation.
+ * Collective when world > 1: set it identically on every rank.  Errors: BV_EINVAL (NULL). */
 bv_status bv_set_jitter(bv_handle* h, int32_t enable);
 
 /* Blocks (over all ranks) that needed jitter in the most recent evaluation
@@ -127,8 +150,9 @@ bv_status bv_jitter_events(const bv_handle* h, int64_t* events);
 bv_status bv_owned_range(const bv_handle* h, int32_t* k_begin, int32_t* k_end);
 
 /* End-to-end variant (host observations in, ℓ out): copies y (n host
- * doubles, in global point-id order) to the device inside the call, then
- * evaluates.  Used to time the whole path with host↔device traffic. */
+ * doubles, in global point-id order, all finite — else BV_EINVAL naming the
+ * first non-finite entry) to the device inside the call, then evaluates.  Used
+ * to time the whole path with host↔device traffic. */
 bv_status bv_loglik_host_y(bv_handle* h, const double* y, const double theta[3], double* loglik);
 
 /* ---- block-Vecchia prediction (Alg. 2; §2.3 :194-240) ----
@@ -159,8 +183,11 @@ typedef struct {
  * m_b + l_b ≤ 235 (the joint triangle lives in shared memory).  Errors:
  * BV_EINVAL (invalid pred plan / θ; message names the first violation),
  * BV_ENOTPD (Σcon of a block not positive definite; bv_last_error's
- * failed_position = the smallest such block id).  Not collective: under
- * multi-GPU any rank may call it alone (the point records are replicated). */
+ * failed_position = the smallest such block id).  Prediction never jitters
+ * (bv_set_jitter applies to bv_loglik* only): Alg. 2 has no fallback and a
+ * singular Σcon means duplicated training locations in a conditioning set.
+ * Not collective: under multi-GPU any rank may call it alone (the point
+ * records are replicated). */
 bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp, double* mean, double* var,
                      double* cov);
 

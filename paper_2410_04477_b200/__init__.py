@@ -31,7 +31,7 @@ _NAMES = {2: "BV_EINVAL", 3: "BV_ENOTPD", 4: "BV_EIO", 5: "BV_ECUDA", 6: "BV_ENC
 EXPORTS = ["bv_version", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_owned_range",
            "bv_loglik_host_y", "bv_last_error", "bv_launches_per_eval", "bv_stream", "bv_last_kernel_ms", "bv_destroy", "bv_partition",
            "bv_fixed_encode", "bv_fixed_decode", "bv_predict", "bv_plan_kmeans", "bv_plan_block_nn",
-           "bv_plan_last_error", "bv_set_jitter", "bv_jitter_events"]
+           "bv_plan_last_error", "bv_set_jitter", "bv_jitter_events", "bv_setup_rank_local", "bv_loglik_acc"]
 
 
 class BVError(RuntimeError):
@@ -74,6 +74,8 @@ def lib():
             L.bv_version.restype = C.c_char_p
             L.bv_nccl_unique_id.argtypes = [C.c_void_p]
             L.bv_setup.argtypes = [C.POINTER(_Plan), C.POINTER(_Dist), C.POINTER(C.c_void_p)]
+            L.bv_setup_rank_local.argtypes = [C.POINTER(_Plan), C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]
+            L.bv_loglik_acc.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
             L.bv_loglik.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
             L.bv_loglik_terms.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_double), C.c_void_p, C.c_void_p]
             L.bv_loglik_host_y.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double)]
@@ -102,7 +104,7 @@ def lib():
             L.bv_plan_last_error.restype = C.c_char_p
             for fn in ("bv_plan_kmeans", "bv_plan_block_nn", "bv_predict", "bv_nccl_unique_id", "bv_setup", "bv_loglik", "bv_loglik_terms", "bv_loglik_host_y",
                        "bv_owned_range", "bv_last_error", "bv_partition", "bv_fixed_encode", "bv_set_jitter",
-                       "bv_jitter_events"):
+                       "bv_jitter_events", "bv_setup_rank_local", "bv_loglik_acc"):
                 getattr(L, fn).restype = C.c_int
             _lib = L
     return _lib
@@ -185,10 +187,13 @@ class BlockVecchia:
     ``plan`` needs numpy-convertible attributes ``locs (n,d) f64, y (n,) f64,
     block_id (n,) i32, order (bc,) i32, nbr_ptr (bc+1,) i64, nbr_idx i32``.
     For world > 1 pass rank/world and the same 128-byte ``nccl_id`` on every
-    rank (see :func:`nccl_unique_id`).
+    rank (see :func:`nccl_unique_id`).  ``rank_local=True`` (tests only) builds
+    rank ``rank`` of ``world`` without a communicator (bv_setup_rank_local): its
+    evaluations return that rank's partial sum.
     """
 
-    def __init__(self, plan, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+    def __init__(self, plan, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                 rank_local: bool = False):
         L = lib()
         self._L = L
         self._h = C.c_void_p()
@@ -204,12 +209,15 @@ class BlockVecchia:
         p = _Plan(self.n, self.d, _ptr(k["locs"]), _ptr(k["y"]), self.bc, _ptr(k["block_id"]), _ptr(k["order"]),
                   _ptr(k["nbr_ptr"]), _ptr(k["nbr_idx"]))
         idbuf = None
-        if world > 1:
+        if world > 1 and not rank_local:
             if nccl_id is None or len(nccl_id) != 128:
                 raise BVError(BV_EINVAL, "world > 1 needs a 128-byte nccl_id")
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
         dist = _Dist(int(device), int(rank), int(world), C.cast(idbuf, C.c_void_p) if idbuf is not None else None)
-        st = L.bv_setup(C.byref(p), C.byref(dist), C.byref(self._h))
+        if rank_local:
+            st = L.bv_setup_rank_local(C.byref(p), int(device), int(rank), int(world), C.byref(self._h))
+        else:
+            st = L.bv_setup(C.byref(p), C.byref(dist), C.byref(self._h))
         self._keep = None  # bv_setup copied everything
         if st:
             msg = C.c_char_p()
@@ -253,6 +261,17 @@ class BlockVecchia:
         self._check(self._L.bv_loglik_terms(self._h, th.ctypes.data, C.byref(out), _ptr(d), _ptr(u)))
         return out.value, d, u
 
+    def loglik_acc(self, theta) -> np.ndarray:
+        """The evaluation's exact fixed-point accumulator (bv_loglik_acc): uint64[8] = six chunk
+        sums, failed-block count, (smallest failing global position << 8 | status).  A non-PD
+        evaluation still returns the accumulator."""
+        th = self._theta(theta)
+        acc = np.zeros(8, dtype=np.uint64)
+        st = self._L.bv_loglik_acc(self._h, th.ctypes.data, acc.ctypes.data)
+        if st not in (BV_OK, BV_ENOTPD):
+            self._check(st)
+        return acc
+
     def set_jitter(self, enable: bool = True):
         """Optional jitter retry for non-PD blocks (bv_set_jitter; reading G15b)."""
         self._check(self._L.bv_set_jitter(self._h, 1 if enable else 0))
@@ -267,10 +286,15 @@ class BlockVecchia:
     def loglik_host_y(self, y, theta) -> float:
         """End-to-end call: host y (global id order) copied in, ℓ back."""
         th = self._theta(theta)
-        if hasattr(y, "data_ptr"):  # torch pinned CPU tensor
+        if hasattr(y, "data_ptr"):  # torch (pinned) CPU tensor: passed by pointer, so check it here
+            import torch
+            if y.dtype != torch.float64 or y.device.type != "cpu" or not y.is_contiguous() or y.numel() != self.n:
+                raise BVError(BV_EINVAL, f"y must be a contiguous CPU float64 tensor of {self.n} elements")
             yp = y.data_ptr()
         else:
             y = np.ascontiguousarray(y, dtype=np.float64)
+            if y.size != self.n:
+                raise BVError(BV_EINVAL, f"y must have {self.n} elements, got {y.size}")
             yp = y.ctypes.data
         out = C.c_double()
         self._check(self._L.bv_loglik_host_y(self._h, yp, th.ctypes.data, C.byref(out)))

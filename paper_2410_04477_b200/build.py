@@ -11,8 +11,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbv.so")
-SOURCES = ["bv_host.cpp", "bv_kernels.cu", "bv_block_v2.cu", "bv_block_v3.cu", "bv_predict.cu", "bv_cv.cu", "bv_plan.cu"]
-HEADERS = ["bv_common.cuh", "matern.cuh", "bessel_k.cuh"]
+SOURCES = ["bv_host.cpp", "bv_kernels.cu", "bv_block_v3.cu", "bv_block_w.cu", "bv_predict.cu", "bv_cv.cu", "bv_plan.cu"]
+HEADERS = ["bv_common.cuh", "matern.cuh", "bessel_k.cuh", "bv_tile.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -51,7 +51,9 @@ def build(force: bool = False, verbose: bool = False, profile_phases: bool = Fal
              "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc]
     # one nvcc per translation unit, in parallel (the v3 kernel's instantiations dominate), then link
     objs = [f"{tmp}.{i}.o" for i in range(len(SOURCES))]
-    procs = [subprocess.Popen(["nvcc", *flags, "-c", os.path.join(CSRC, f), "-o", o]) for f, o in zip(SOURCES, objs)]
+    split = lambda f: ["-split-compile=4"] if f.startswith("bv_block_v") else []
+    procs = [subprocess.Popen(["nvcc", *flags, *split(f), "-c", os.path.join(CSRC, f), "-o", o])
+             for f, o in zip(SOURCES, objs)]
     rcs = [p.wait() for p in procs]
     try:
         if any(rcs):

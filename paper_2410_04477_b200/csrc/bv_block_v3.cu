@@ -34,40 +34,13 @@
 namespace bv {
 namespace v3 {
 
-// Panel solve L(I,J) = C(I,J) L_JJ⁻ᵀ: 0 = row substitution (one row per
-// thread, residual-corrected divisions); 1 = DMMA with the explicit L_JJ⁻¹
-// plus one FP64 refinement step; 2 = DMMA with L_JJ⁻¹ only (A/B only: loses
-// accuracy on ill-conditioned tiles, fails the κ-aware parity rule at c3).
-#ifndef BV_TRSM
-#define BV_TRSM 1
-#endif
-// Refinement of the DMMA panel solve only where L_JJ is ill-conditioned: the
-// explicit-inverse product C L_JJ⁻ᵀ has relative error ~ u·κ(L_JJ), which for a
-// tile whose pivots L_jj spread by less than BV_REF_RATIO (a lower bound on
-// κ(L_JJ) that the Cholesky pivots of a nearly singular tile expose) is at the
-// level of substitution; above it the FP64 refinement step runs.  The flag is
-// per CTA and panel (uniform: no divergence).  0 = always refine.
-// Measured at c4 (gpurun_out/ab5, round 1): always refining 199 evals/s; ratio
-// 16: 188; never: 193 (and fails c3 parity) — the panel solves are not on the
-// kernel's critical resource, so the default keeps the refinement everywhere.
-#ifndef BV_REF_RATIO
-#define BV_REF_RATIO 0
-#endif
-// Update-warp panel solves (tiles I ≥ J+2): 0 = row substitution against the
-// row-major L_JJ (DFMA; 26 FP64-pipe cycles per tile instead of the 96 of three
-// DMMA tile products), 1 = same as the chain (DMMA + refinement).  The chain's
-// own L(J+1,J) is on the critical path and keeps the short DMMA dependency chain.
-#ifndef BV_TRSM_U
-#define BV_TRSM_U BV_TRSM
-#endif
-
-// Measured at c4 (gpurun_out/ab7): kW = 4 (5 CTAs/SM) 197 evals/s, 5 → 187,
-// 6 → 180, 8 (2 CTAs/SM) → 166.  Resident CTAs vs throughput at kW = 4
-// (ab6, shared memory padded): 1/2/3/4/5 CTAs per SM → 73/127/164/187/199.
-#ifndef BV_KW
-#define BV_KW 4
-#endif
-constexpr int kW = BV_KW;  // warps per CTA: 1 chain warp + kW−1 update warps
+// Panel solves L(I,J) = C(I,J) L_JJ⁻ᵀ are DMMA products with the explicit L_JJ⁻¹
+// plus one FP64 refinement step (a bare product with the inverse loses accuracy
+// on ill-conditioned tiles and fails the κ-aware parity rule at c3; row
+// substitution on the update warps measured 7 % slower, round 1).
+// 4 warps per CTA (1 chain + 3 update): measured at c4, 5/6/8 warps per CTA gave
+// 187/180/166 evals/s against 197 (round 1).
+constexpr int kW = 4;  // warps per CTA: 1 chain warp + kW−1 update warps
 constexpr int kNT = kW * 32;
 constexpr int kBarG = 1, kBarF = 2, kBarE = 3, kBarU = 4, kBarH = 5;  // named barriers (0 = __syncthreads)
 
@@ -101,37 +74,6 @@ __device__ __forceinline__ double neg(double x) {
 __device__ __forceinline__ void bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
-// 8-double rows moved as four 16-byte chunks in a rotated order (row g touches
-// chunk (k + g/2) mod 4 at step k): the 8 rows of a tile hit 8 distinct bank
-// groups.  Layout unchanged (chunk q at offset 2q).
-__device__ __forceinline__ double2 sel4(const double2 (&v)[4], int i) {
-  const double2 a = (i & 1) ? v[1] : v[0];
-  const double2 b = (i & 1) ? v[3] : v[2];
-  return (i & 2) ? b : a;
-}
-__device__ __forceinline__ void ld_row_rot(const double* row, int rot, double (&c)[8]) {
-  double2 t[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) t[k] = lds2(row + 2 * ((k + rot) & 3));
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const double2 v = sel4(t, (q - rot) & 3);
-    c[2 * q] = v.x;
-    c[2 * q + 1] = v.y;
-  }
-}
-// store row x in DMMA fragment order: chunk q holds (x[q], x[q+4])
-__device__ __forceinline__ void st_row_frag_rot(double* row, int rot, const double (&x)[8]) {
-  const double2 ch[4] = {make_double2(x[0], x[4]), make_double2(x[1], x[5]), make_double2(x[2], x[6]),
-                         make_double2(x[3], x[7])};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int q = (k + rot) & 3;
-    const double2 v = sel4(ch, q);
-    sts2(row + 2 * q, v.x, v.y);
-  }
-}
-
 struct Layout {
   int P, dtile, ptile, linv, lfr, lrow, rinv, misc, theta, etab, slots, tab, total_bytes;
   __host__ __device__ Layout(int TImax, int cap) {
@@ -140,15 +82,10 @@ struct Layout {
     ptile = dtile + 64;      // next diagonal tile's partial P(J+1,J+1) (update warps → chain)
     linv = ptile + 64;       // [2][64] L_JJ⁻¹ in DMMA fragment order (0 on padding rows)
     lfr = linv + 128;        // [2][64] L_JJ in DMMA fragment order
-    lrow = lfr + 128;        // [2][64] L_JJ row-major (L_jj on the diagonal) for update-warp row solves
-#if BV_TRSM_U == 0 && BV_TRSM != 0
-    rinv = lrow + 128;       // [2][8] 1/L_jj
-    misc = rinv + 16;        // [1] chain quad, [2] fail, [3] chain warp, [4] logdet, [5..7] update-warp quads
-#else
-    rinv = lrow;  // (unused: no extra buffers unless BV_TRSM_U = 0 with a DMMA chain)
-    misc = lrow;
-#endif
-    theta = misc + ((kW + 7) & ~1);  // Theta (≤ 20 doubles); misc[4+kW+(J&1)] = refine flag of panel J
+    lrow = lfr + 128;        // (no row-major copy: panel solves are all DMMA)
+    rinv = lrow;
+    misc = lrow;             // [1] chain quad, [2] fail, [3] chain warp, [4] logdet, [5..7] update-warp quads
+    theta = misc + ((kW + 7) & ~1);  // Theta (≤ 20 doubles)
     etab = theta + 20;       // 2^{−j/64}, j = 0..63 (exp_neg)
     slots = etab + 64;       // cap tiles
     tab = slots + 64 * cap;  // int16 slot table (TImax²)
@@ -176,41 +113,23 @@ __device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec
   return (r == N) ? pc.v : v;  // the y row; padding entries are 0 by construction (far points)
 }
 
-// Row solve x = c L_JJ⁻ᵀ against the published diagonal factor (row-major
-// lower with L_jj on the diagonal, 1/L_jj in ri): scaled by 1/L_kk, then one
-// residual correction per entry.
-__device__ __forceinline__ void row_solve(const double (&c)[8], const double* dl, const double* ri, double (&x)[8]) {
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    double tv = c[k];
-#pragma unroll
-    for (int kk = 0; kk < k; ++kk) tv = fma(-x[kk], dl[8 * k + kk], tv);
-    const double xk = tv * ri[k];
-    x[k] = fma(fma(-xk, dl[9 * k], tv), ri[k], xk);
-  }
-}
-
 // In-lane Cholesky of the 8×8 tile t (row-major lower, every lane holds it),
-// then (BV_TRSM ≥ 1) L_JJ⁻¹ by columns (lane j solves L x = e_j).  Lanes 0..7 publish column
+// then L_JJ⁻¹ by columns (lane j solves L x = e_j).  Lanes 0..7 publish column
 // j of both L_JJ (lf) and L_JJ⁻¹ (li) in DMMA fragment order: element (i,k) at
 // 2(4i + (k&3)) + (k>>2).  Padding pivots (j ≥ N − 8J) get 1/L_jj = 0, so
 // their rows of L_JJ⁻¹ — and with them the padding columns of every
 // L(I,J) = C(I,J) L_JJ⁻ᵀ — are zero.
-__device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, double* lr, double* ri, int J,
-                                            int m, int N, int lane, double pfloor, double& prod, int& nbad,
-                                            double& qd, double& spread) {
+__device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, int J, int m, int N, int lane,
+                                            double pfloor, double jit, double& prod, int& nbad, double& qd) {
   const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
   double a[8][8], rr[8];
-  double pmax = 0.0, pmin = 1.7976931348623157e308;
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int k = 0; k <= i; ++k) a[i][k] = t[8 * i + k];
-#ifdef BV_ABL_CHAIN  // timing ablation only: no pivot chain (results meaningless)
+  // optional jitter mode (reading G15b): ε·σ² on every real diagonal entry of the joint matrix
 #pragma unroll
-  for (int j = 0; j < 8; ++j) rr[j] = a[j][j];
-  if (false)
-#endif
+  for (int i = 0; i < 8; ++i) a[i][i] += (i < nreal) ? jit : 0.0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     double p = a[j][j];
@@ -224,25 +143,16 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
     const double lv = p * r;
     rr[j] = rv;
     a[j][j] = lv;
-    if (real) {
-      pmax = fmax(pmax, p);
-      pmin = fmin(pmin, p);
-    }
 #pragma unroll
     for (int i = j + 1; i < 8; ++i) {
       const double x = a[i][j] * rv;
-#ifdef BV_CHAIN_NOCORR  // A/B only: drop the correction step (fewer chain instructions, less accurate)
-      a[i][j] = x;
-#else
       a[i][j] = fma(fma(-x, lv, a[i][j]), rv, x);
-#endif
     }
 #pragma unroll
     for (int i = j + 1; i < 8; ++i)
 #pragma unroll
       for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
   }
-  spread = pmax / pmin;  // (max L_jj / min L_jj)²
 #pragma unroll
   for (int i = 1; i < 8; ++i)
     if (i == yr) {
@@ -251,22 +161,6 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
         if (k >= jm) qd = fma(a[i][k], a[i][k], qd);
     }
   const int j = lane & 7;
-#if BV_TRSM == 0
-  // substitution mode: lf = L_JJ row-major (L_jj on the diagonal), li[0..7] = 1/L_jj
-  if (lane < 8) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      double l = 0.0;
-#pragma unroll
-      for (int k = 0; k <= i; ++k) l = (k == j) ? a[i][k] : l;
-      lf[8 * i + j] = l;
-    }
-    double r = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r = (k == j) ? rr[k] : r;
-    li[j] = r;
-  }
-#else
   // column j = lane & 7 of L⁻¹: x_i = (δ_ij − Σ_{k<i} L_ik x_k) / L_ii
   double x[8];
 #pragma unroll
@@ -285,20 +179,8 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
 #pragma unroll
       for (int k = 0; k <= i; ++k) l = (k == j) ? a[i][k] : l;
       lf[o] = l;
-#if BV_TRSM_U == 0
-      lr[8 * i + j] = l;
-#endif
     }
-#if BV_TRSM_U == 0
-    double r = 0.0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r = (k == j) ? rr[k] : r;
-    ri[j] = r;
-#endif
   }
-  (void)lr;
-  (void)ri;
-#endif
 }
 
 // L(I,J) = C(I,J) L_JJ⁻ᵀ for one tile, in place (one warp): C is row-major,
@@ -310,7 +192,7 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
 // Returns the lane's two results (row g, columns 2t, 2t+1) for the y-row term.
 template <int NT>
 __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 bi, double2 bl, int g, int t,
-                                            double2 (&out)[NT], bool refine = true) {
+                                            double2 (&out)[NT]) {
   double x0[NT], x1[NT], cc0[NT], cc1[NT];
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
@@ -324,8 +206,6 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     dmma884(x0[i], x1[i], c1, bi.y);
   }
   __syncwarp();
-#if BV_TRSM == 1
-  if (refine) {
 #pragma unroll
   for (int i = 0; i < NT; ++i) sts2(tile[i] + 8 * g + 2 * t, x0[i], x1[i]);
   __syncwarp();
@@ -346,12 +226,6 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     dmma884(x0[i], x1[i], ra[4], bi.y);
   }
   __syncwarp();
-  }
-#else
-  (void)bl;
-  (void)cc0;
-  (void)cc1;
-#endif
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
     tile[i][8 * g + 2 * ((2 * t) & 3) + (t >> 1)] = x0[i];
@@ -359,10 +233,10 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     out[i] = make_double2(x0[i], x1[i]);
   }
 }
-__device__ __forceinline__ double2 tile_trsm(double* tile, double2 bi, double2 bl, int g, int t, bool refine = true) {
+__device__ __forceinline__ double2 tile_trsm(double* tile, double2 bi, double2 bl, int g, int t) {
   double* const tl[1] = {tile};
   double2 o[1];
-  tile_trsm_n<1>(tl, bi, bl, g, t, o, refine);
+  tile_trsm_n<1>(tl, bi, bl, g, t, o);
   return o[0];
 }
 
@@ -382,12 +256,6 @@ __device__ __forceinline__ double* slot_at(double* base, unsigned slot) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(base) + (slot << 9));
 }
 
-// A/B: split the GEMM accumulator chain when a warp has ≤ BV_GEMM_SPLIT tiles (0 = never).
-// Measured (gpurun_out/ab20): c4 214.5/214.1 evals/s at 2/5 vs 214.5 without; c5 m=30 no
-// change either: the late-panel DMMA chains are not the critical path.
-#ifndef BV_GEMM_SPLIT
-#define BV_GEMM_SPLIT 0
-#endif
 template <int NS, int MAXT>
 __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
                                        int uw, int lane) {
@@ -397,31 +265,6 @@ __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots
   const uint16_t* tI[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) tI[s] = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (kW - 1) * s) * TI;
-#if BV_GEMM_SPLIT
-  if constexpr (NS <= BV_GEMM_SPLIT) {
-    // few tiles per warp (late panels): the accumulator chain of 2J dependent DMMAs is
-    // the phase's latency; split it over the two k-halves (two independent chains)
-    double T[NS][2];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) T[s][0] = T[s][1] = 0.0;
-#pragma unroll 2
-    for (int K = 0; K < J; ++K) {
-      const double2 b = lds2(slot_at(sl, tJ[K]));
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        const double2 a = lds2(slot_at(sl, tI[s][K]));
-        dmma884(S[s][0], S[s][1], a.x, b.x);
-        dmma884(T[s][0], T[s][1], a.y, b.y);
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      S[s][0] += T[s][0];
-      S[s][1] += T[s][1];
-    }
-    return;
-  }
-#endif
 #pragma unroll 2
   for (int K = 0; K < J; ++K) {
     const double2 b = lds2(slot_at(sl, tJ[K]));
@@ -435,30 +278,14 @@ __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots
 }
 
 
-// Half-tiles of generation in flight per update warp.  Measured (gpurun_out/ab20):
-// 2 → 213.7/215.2 evals/s at c4 vs 214.0/214.9 at 1 (noise); kept at 1.
-// (Same run: BV_TRSM_U=0, row-substitution panel solves on the update warps,
-// 197.8/199.2 — the DMMA + refinement solve stays.)
-#ifndef BV_V3_GEN_UNROLL
-#define BV_V3_GEN_UNROLL 1
-#endif
-constexpr int kV3GenUnroll = BV_V3_GEN_UNROLL;  // half-tiles in flight per update warp
+// One half-tile of generation in flight per update warp (two measured the same, round 1).
+constexpr int kV3GenUnroll = 1;
 
 // CTAs per SM the register allocation targets: shared memory admits 5 blocks
 // of TI ≤ 16 (MAXT ≤ 5, the bulk of c3/c4) and 4 of TI 17-18; 5 × 128 threads
 // caps registers at 102 (a few spills in the chain warp's in-lane factor,
 // measured +2.5 % at c4 over 4 CTAs with none).
-#ifndef BV_MINB_SMALL
-#define BV_MINB_SMALL 5
-#endif
-// MAXT ≤ 2 (TI ≤ 7, N ≤ 55: c5 at m = 30): shared memory admits far more CTAs,
-// but 6 or 8 per SM (spilling) measured the same 400 evals/s at c5 m = 30 (ab8).
-#ifndef BV_MINB_TINY
-#define BV_MINB_TINY 5
-#endif
-constexpr int v3_minb(int maxt) {
-  return maxt >= 16 ? 2 : kW == 4 ? (maxt <= 2 ? BV_MINB_TINY : maxt <= 5 ? BV_MINB_SMALL : 4) : (kW <= 6 ? 3 : 2);
-}
+constexpr int v3_minb(int maxt) { return maxt >= 16 ? 2 : maxt <= 5 ? 5 : 4; }
 // Joint sizes beyond what shared memory holds (TI > 37, N > 295: the paper's
 // conditioning sets reach 420-450) keep the same schedule
 // with the tile slots in a global-memory scratch (L1/L2-resident) instead of
@@ -474,7 +301,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
                    const int32_t* __restrict__ tab_off, const double* __restrict__ exp_tab, int TImax, int cap,
                    double* __restrict__ out_u, double* __restrict__ out_d, unsigned long long* __restrict__ acc,
                    int k_begin, double* __restrict__ gslots, int nblocks, const double* __restrict__ pre,
-                   const int64_t* __restrict__ pre_off) {
+                   const int64_t* __restrict__ pre_off, double jit) {
   constexpr bool GS = MAXT >= kGsMaxT;
   extern __shared__ __align__(16) double smem[];
   const Layout Ly(TImax, GS ? 0 : cap);
@@ -521,13 +348,6 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   }
   if (tid < 4) misc[tid] = 0.0;
   __syncthreads();
-#ifdef BV_CHAIN_SMSP0
-  {  // the chain warp is the one on SM sub-partition 0
-    unsigned wid;
-    asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
-    if (lane == 0 && (wid & 3u) == 0u) misc[3] = (double)warp;
-  }
-#endif
   // default: the chain is warp 0 — the hardware rotates co-resident CTAs'
   // warps over the four SM sub-partitions (tools/peaks/wid_probe), so the
   // chains of the ~4 resident blocks land on different FP64 pipes
@@ -553,24 +373,13 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       double* li = linv + 64 * (J & 1);
       double* lj = lfr + 64 * (J & 1);
       P3_T(t0);
-      double spread;
-      factor_tile(dtile, lj, li, smem + Ly.lrow + 64 * (J & 1), smem + Ly.rinv + 8 * (J & 1), J, m, N, lane, pfloor,
-                  pm, nbad, qd_in, spread);  // a4/a7
-#if BV_REF_RATIO > 0
-      const bool refine = !(spread <= (double)BV_REF_RATIO * (double)BV_REF_RATIO);
-      if (lane == 0) misc[4 + kW + (J & 1)] = refine ? 1.0 : 0.0;
-#else
-      constexpr bool refine = true;
-      (void)spread;
-#endif
+      factor_tile(dtile, lj, li, J, m, N, lane, pfloor, jit, pm, nbad, qd_in);  // a4/a7
       int ex;
       pm = frexp(pm, &ex);
       pe += ex;
       __syncwarp();
-#if BV_TRSM != 0
       const double2 bi = lds2(li + 2 * lane);  // this lane's fragments of L_JJ⁻¹ and L_JJ
       const double2 bl = lds2(lj + 2 * lane);
-#endif
       P3_ADD(0, t0);
       P3_T(t1);
       // U finished iteration J−1 (so it has consumed G, F, H of J−1: a named
@@ -584,19 +393,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         // TJ, below the last diagonal tile — its solve is this warp's (U only
         // handles tiles I ≥ J+2)
         if (TI > TJ) {
-#if BV_TRSM == 0
-          if (lane == (N & 7)) {
-            double c[8], x[8];
-            ld_row_rot(slots + 64 * tab[TJ * TI + J] + 8 * (N & 7), (N & 7) >> 1, c);
-            row_solve(c, lj, li, x);
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
-          }
-#else
-          const double2 d = tile_trsm(slot_at(slots, tabu[TJ * TI + J]), bi, bl, g, t, refine);
+          const double2 d = tile_trsm(slot_at(slots, tabu[TJ * TI + J]), bi, bl, g, t);
           if (g == (N & 7)) qd_t += yrow_sq(d, J, t, m, N);
-#endif
         }
         break;
       }
@@ -604,22 +402,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       // L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ (a5/a6)
       double* tj = slot_at(slots, tabu[(J + 1) * TI + J]);
       {
-#if BV_TRSM == 0
-        double* row = tj + 8 * (lane & 7);  // row i = lane & 7 (lanes 8..31 shadow)
-        double c[8], x[8];
-        ld_row_rot(row, (lane & 7) >> 1, c);
-        row_solve(c, lj, li, x);
-        if (8 * (J + 1) + (lane & 7) == N && lane < 8) {  // the y row: u += Σ_{j≥m} z_j²
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (8 * J + k >= m && 8 * J + k < N) qd_t = fma(x[k], x[k], qd_t);
-        }
-        __syncwarp();
-        if (lane < 8) st_row_frag_rot(row, (lane & 7) >> 1, x);
-#else
-        const double2 d = tile_trsm(tj, bi, bl, g, t, refine);
+        const double2 d = tile_trsm(tj, bi, bl, g, t);
         if (8 * (J + 1) + g == N) qd_t += yrow_sq(d, J, t, m, N);  // the y row: u += Σ_{j≥m} z_j²
-#endif
       }
       __syncwarp();
       const double2 lf = lds2(tj + 2 * lane);  // read before F: slot may be recycled
@@ -702,56 +486,24 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       P3_ADD(7, u7);
       P3_T(u8);
       {
-#if BV_TRSM_U == 0
-        // L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2, one row per update thread (a5/a6)
-#if BV_TRSM == 0
-        const double* dl = lfr + 64 * (J & 1);
-        const double* ri = linv + 64 * (J & 1);
-#else
-        const double* dl = smem + Ly.lrow + 64 * (J & 1);
-        const double* ri = smem + Ly.rinv + 8 * (J & 1);
-#endif
-        const int rows = (TI - J - 2) * 8;
-        const int utid = (uw - 1) * 32 + lane;
-#pragma unroll 1
-        for (int rr = utid; rr < rows; rr += (kW - 1) * 32) {
-          const int I = J + 2 + (rr >> 3), gg = rr & 7;
-          double* row = slots + 64 * tab[I * TI + J] + 8 * gg;
-          double c[8], x[8];
-          ld_row_rot(row, gg >> 1, c);
-          row_solve(c, dl, ri, x);
-          if (8 * I + gg == N) {  // the y row: u += Σ_{j≥m} z_j² (a8)
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (8 * J + k >= m && 8 * J + k < N) qd_u = fma(x[k], x[k], qd_u);
-          }
-          st_row_frag_rot(row, gg >> 1, x);
-        }
-#else
         // L(I,J) = C(I,J) L_JJ⁻ᵀ for this warp's tiles I = J+u+3s > J+1 (a5/a6)
         const double2 bi = lds2(linv + 64 * (J & 1) + 2 * lane);
         const double2 bl = lds2(lfr + 64 * (J & 1) + 2 * lane);
-#if BV_REF_RATIO > 0
-        const bool refine = misc[4 + kW + (J & 1)] != 0.0;
-#else
-        constexpr bool refine = true;
-#endif
-        // two tiles in flight: their DMMA / shared-memory round trips interleave
+          // two tiles in flight: their DMMA / shared-memory round trips interleave
 #pragma unroll 1
         for (int I = J + uw + (uw == 1 ? kW - 1 : 0); I < TI; I += 2 * (kW - 1)) {
           const int I2 = I + kW - 1;
           if (I2 < TI) {
             double* const tl[2] = {slot_at(slots, tabu[I * TI + J]), slot_at(slots, tabu[I2 * TI + J])};
             double2 d[2];
-            tile_trsm_n<2>(tl, bi, bl, g, t, d, refine);
+            tile_trsm_n<2>(tl, bi, bl, g, t, d);
             if (8 * I + g == N) qd_u += yrow_sq(d[0], J, t, m, N);  // the y row (a8)
             if (8 * I2 + g == N) qd_u += yrow_sq(d[1], J, t, m, N);
           } else {
-            const double2 d = tile_trsm(slot_at(slots, tabu[I * TI + J]), bi, bl, g, t, refine);
+            const double2 d = tile_trsm(slot_at(slots, tabu[I * TI + J]), bi, bl, g, t);
             if (8 * I + g == N) qd_u += yrow_sq(d, J, t, m, N);
           }
         }
-#endif
       }
       P3_ADD(8, u8);
       // (no U barrier here: F below is a full barrier of the update warps, so
@@ -833,18 +585,11 @@ int v3_maxt_for(int TI) {
   return -1;
 }
 
-#ifndef BV_MIN_SMEM  // A/B only: pad the dynamic shared memory to cap resident CTAs per SM
-#define BV_MIN_SMEM 0
-#endif
 bool v3_global_slots(int TI) { return v3_maxt_for(TI) >= v3::kGsMaxT; }
 
 size_t v3_smem_bytes(int TImax, int cap) {
   const size_t b = (size_t)v3::Layout(TImax, v3_global_slots(TImax) ? 0 : cap).total_bytes;
-#if BV_MIN_SMEM > 0
-  return b < (size_t)BV_MIN_SMEM ? (size_t)BV_MIN_SMEM : b;
-#else
   return b;
-#endif
 }
 
 template <int MAXT>
@@ -882,11 +627,11 @@ static void v3_launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, c
                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                            const int16_t* tabs, const int32_t* tab_off, const double* etab, int TImax, int cap,
                            double* u, double* d, unsigned long long* acc, int k_begin, double* gslots, int grid,
-                           const double* pre, const int64_t* pre_off) {
+                           const double* pre, const int64_t* pre_off, double jit) {
 #define BV_K(KD)                                                                                             \
   v3::bv_block_v3_kernel<MAXT, KD><<<grid, v3::kNT, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, \
                                                                TImax, cap, u, d, acc, k_begin, gslots, nblocks, \
-                                                               pre, pre_off)
+                                                               pre, pre_off, jit)
   switch (kind) {
     case 0: BV_K(0); break;
     case 1: BV_K(1); break;
@@ -901,7 +646,7 @@ cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStrea
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
                             unsigned long long* acc, int k_begin, double* gslots, int gs_grid, const double* pre,
-                            const int64_t* pre_off) {
+                            const int64_t* pre_off, double jit) {
   if (nblocks == 0) return cudaSuccess;
   const size_t smem = v3_smem_bytes(TImax, cap);
   const int grid = v3_global_slots(TImax) ? (nblocks < gs_grid ? nblocks : gs_grid) : nblocks;
@@ -909,7 +654,7 @@ cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStrea
 #define BV_MT(MT)                                                                                          \
   case MT:                                                                                                 \
     v3_launch_kind<MT>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, d, \
-                       acc, k_begin, gslots, grid, pre, pre_off);                                          \
+                       acc, k_begin, gslots, grid, pre, pre_off, jit);                                     \
     break;
     BV_MT(1) BV_MT(2) BV_MT(3) BV_MT(4) BV_MT(5) BV_MT(6) BV_MT(8) BV_MT(10) BV_MT(12) BV_MT(16) BV_MT(20)
 #undef BV_MT

@@ -25,11 +25,6 @@
 #include "bv_common.cuh"
 
 namespace bv {
-size_t v1_smem_bytes(int Nmax);
-cudaError_t prepare_block_v1(int Nmax);
-cudaError_t launch_block_v1(int nblocks, int Nmax, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
-                            const BlockDesc* desc, const int32_t* list, const Theta* th, double* u, double* d,
-                            unsigned long long* acc, int k_begin, double jit = 0.0);
 cudaError_t launch_cv(int kind, int count, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                       const BlockDesc* desc, const int32_t* list, const Theta* th, const double* etab, double* u,
                       double* d, unsigned long long* acc, int k_begin);
@@ -39,57 +34,52 @@ cudaError_t launch_predict(int nblocks, size_t smem, cudaStream_t s, const Point
                            const int32_t* nbr, const BlockDesc* desc, const Theta* th, const int64_t* cov_off,
                            double* mean, double* var, double* cov, int32_t* status);
 cudaError_t launch_scatter_y(const double* y, const int32_t* perm_of_id, int64_t n, PointRec* pts, cudaStream_t s);
-int v2_maxt_for(int TI);
 int v3_maxt_for(int TI);
 size_t v3_smem_bytes(int TImax, int cap);
 cudaError_t prepare_block_v3(size_t max_smem);
 cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
                             const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                             const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid,
-                            const double* pre = nullptr, const int64_t* pre_off = nullptr);
+                            unsigned long long* acc, int k_begin, double* gslots, int gs_grid, const double* pre,
+                            const int64_t* pre_off, double jit);
 cudaError_t launch_pregen(int nblocks, int chunks, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
                           const BlockDesc* desc, const Theta* th, const double* etab, const int64_t* pre_off,
                           double* pre);
 bool v3_global_slots(int TI);
-int debug_phase_cycles(unsigned long long* out, int reset);
 int debug_v3_cycles(unsigned long long* out, int reset);
-size_t v2_smem_bytes(int TImax, int cap);
-cudaError_t prepare_block_v2(size_t max_smem);
-cudaError_t launch_block_v2(int kind, int nblocks, int TImax, int cap, cudaStream_t s, const PointRec* pts,
-                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
-                            const int16_t* tabs, const int32_t* tab_off, const double* etab, double* u, double* d,
-                            unsigned long long* acc, int k_begin);
+int w_max_ti();
+cudaError_t prepare_block_w();
+cudaError_t launch_block_w(int kind, int nblocks, int TI, cudaStream_t s, const PointRec* pts, const int32_t* nbr,
+                           const BlockDesc* desc, const int32_t* list, const Theta* th, const double* etab, double* u,
+                           double* d, unsigned long long* acc, int k_begin, const double* pre, const int64_t* pre_off,
+                           double jit);
 }  // namespace bv
 
 namespace {
-constexpr int kBucketWidth = 16;
 constexpr size_t kSmemOptin = 232448;  // B200 per-block opt-in shared memory
 
+// The block kernels.  Positions are grouped into buckets by kernel and tile
+// rows TI = ⌈(N+1)/8⌉ (N = m + l, the y row appended).
+enum KernelKind : int { kKernCV = 0, kKernW = 1, kKernV3 = 2 };
 struct Bucket {
-  int Nmax, count, offset;  // v1: Nmax = joint size bound; v2: Nmax = tile rows TI
-  int cap;                  // v2: L slots for this TI
-  size_t gs_off = 0;        // v3 with global slots (TI > 37): this bucket's scratch offset (doubles)
+  int TI, count, offset;  // TI = 0 for the classic-Vecchia kernel
+  int cap;                // v3: tile slots for this TI
+  size_t gs_off = 0;      // v3 with global slots (TI > 37): this bucket's scratch offset (doubles)
+  int kern = kKernV3;
 };
 
-// Slot tables for the v2 kernel (bv_block_v2.cu).  Every tile of column K
-// lives in one shared-memory slot from its generation (C, row-major) through
-// its in-place triangular solve (L, fragment order) until its last use.  For a
-// block with TI tile rows and TJ column panels: column 0 is generated first;
-// iteration J generates column J+1 (tiles I ≥ J+1) at its start, after
-// freeing row J's L tiles (last read in iteration J−1) and the diagonal tile
-// (J−1,J−1) (consumed by iteration J−1's factorisation).  A LIFO free list
-// replays that schedule; slot[I·TI + K] is the slot of tile (I,K).
-// off[2·TI + (TI−TJ)] indexes the table of each (TI, TJ) pair (TI − TJ ∈
-// {0, 1}); cap[TI] = the most slots live at once.
+// Slot tables of the large-block kernel (bv_block_v3.cu).  Every tile of column
+// K lives in one shared-memory slot from its generation (C, row-major) through
+// its in-place triangular solve (L, fragment order) until its last use; diagonal
+// tiles never occupy a slot.  Column 0 (I ≥ 1) first; iteration J frees row J's
+// tiles except L(J,J−1), plus L(J−1,J−2), then generates column J+1's tiles
+// I ≥ J+2.  A LIFO free list replays that schedule; slot[I·TI + K] is the slot
+// of tile (I,K).  off[2·TI + (TI−TJ)] indexes the table of each (TI, TJ) pair
+// (TI − TJ ∈ {0, 1}); cap[TI] = the most slots live at once.
 struct SlotTables {
   std::vector<int16_t> tabs;
   std::vector<int32_t> off;
   std::vector<int> cap;
-  // v3 schedule (bv_block_v3.cu): diagonal tiles never occupy a slot; column 0
-  // (I ≥ 1) first; iteration J frees row J's tiles except L(J,J−1), plus
-  // L(J−1,J−2), and then generates column J+1's tiles I ≥ J+2.
-  bool v3 = true;
   void build(int TImax) {
     off.assign(2 * (size_t)(TImax + 1), 0);
     cap.assign((size_t)TImax + 1, 0);
@@ -115,25 +105,14 @@ struct SlotTables {
           --live;
           freel.push_back(v);
         };
-        if (v3) {
-          for (int I = 1; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
-          for (int J = 0; J + 1 < TJ; ++J) {
-            // L(J,J−1) is the b operand of iteration J−1's final term, which a
-            // slow update warp may still be reading while a fast one generates
-            // column J+1: it is released one iteration later (after the U
-            // barrier of iteration J has separated the two)
-            for (int K = 0; K + 1 < J; ++K) release(t[(size_t)J * TI + K]);
-            if (J >= 2) release(t[(size_t)(J - 1) * TI + J - 2]);
-            for (int I = J + 2; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
-          }
-        } else {
-          for (int I = 0; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
-          for (int J = 0; J < TJ; ++J) {
-            if (J >= 1) release(t[(size_t)(J - 1) * TI + (J - 1)]);
-            for (int K = 0; K < J; ++K) release(t[(size_t)J * TI + K]);
-            if (J + 1 < TJ)
-              for (int I = J + 1; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
-          }
+        for (int I = 1; I < TI; ++I) t[(size_t)I * TI + 0] = alloc();
+        for (int J = 0; J + 1 < TJ; ++J) {
+          // L(J,J−1) is the b operand of iteration J−1's final term, which a slow
+          // update warp may still be reading while a fast one generates column J+1:
+          // it is released one iteration later (after iteration J's U barrier)
+          for (int K = 0; K + 1 < J; ++K) release(t[(size_t)J * TI + K]);
+          if (J >= 2) release(t[(size_t)(J - 1) * TI + J - 2]);
+          for (int I = J + 2; I < TI; ++I) t[(size_t)I * TI + J + 1] = alloc();
         }
         tabs.insert(tabs.end(), t.begin(), t.end());
         cap[TI] = std::max(cap[TI], std::max(most, 1));
@@ -168,7 +147,10 @@ struct bv_handle {
   double* d_gslots = nullptr;  // tile-slot scratch of the global-slot buckets (joint sizes > 295)
   int gs_grid = 0;             // persistent CTAs per global-slot bucket launch
   int32_t* d_tab_off = nullptr;
-  bool use_v1 = false, use_v2 = false;
+  bool local = false;                      // test-only rank-local handle (bv_setup_rank_local): no communicator
+  int wmax = 0;                            // largest TI run by the warp-per-block kernel
+  std::vector<int> cap_of;                 // v3 slot capacity by TI
+  std::vector<size_t> gsoff_of;            // v3 global-slot scratch offset by TI (TI > 37)
   bv::Theta* h_theta = nullptr;            // pinned
   unsigned long long* h_acc = nullptr;     // pinned
   cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;  // around the block kernels (graph event nodes)
@@ -184,7 +166,6 @@ struct bv_handle {
   std::vector<int32_t> h_N;                  // joint size N_q = l + m per local position
   int32_t* d_jlist = nullptr;                // failed positions being retried
   unsigned long long* d_jacc = nullptr;      // the retry's own accumulator (kAccSlots) + 3 allreduce slots
-  int v1_ready = 0;                          // largest N prepare_block_v1 was called for
   // general-ν pre-generation (small plans): packed Σ triangles, offsets per local position
   double* d_pre = nullptr;
   int64_t* d_pre_off = nullptr;
@@ -250,10 +231,13 @@ void fill_general_nu(bv::Theta& t, double nu) {
   t.gen[6] = (double)fact;
 }
 
+// σ², β finite and > 0; ν ∈ {½, 3/2, 5/2} (closed forms) or ν ∈ [0.2, 3], the range the
+// device K_ν evaluator is validated on (bessel_k.cuh; the MLE box of SURVEY §8d).
 bool theta_valid(const double* th) {
   for (int i = 0; i < 3; ++i)
     if (!(th[i] > 0.0) || !std::isfinite(th[i])) return false;
-  return true;
+  const double nu = th[2];
+  return nu == 0.5 || nu == 1.5 || nu == 2.5 || (nu >= 0.2 && nu <= 3.0);
 }
 
 // ν-only table of the x > 2 K_ν evaluators (bessel_k.cuh), long double:
@@ -332,6 +316,24 @@ bv_status upload(bv_handle* h, T** dst, const T* src, size_t count) {
   BV_CUDA(h, cudaMalloc((void**)dst, count * sizeof(T)));
   if (src) BV_CUDA(h, cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyHostToDevice));
   return BV_OK;
+}
+
+// One bucket (or a retry group) of positions through its kernel family.
+cudaError_t launch_bucket(bv_handle* h, const Bucket& b, int kind, cudaStream_t st, const int32_t* list, int count,
+                          unsigned long long* acc, double jit) {
+  switch (b.kern) {
+    case kKernCV:
+      return bv::launch_cv(kind == 4 ? bv::kNuGeneral : kind, count, st, h->d_pts, h->d_nbr, h->d_desc, list,
+                           h->d_theta, h->d_exptab, h->d_u, h->d_d, acc, h->kb);
+    case kKernW:
+      return bv::launch_block_w(kind, count, b.TI, st, h->d_pts, h->d_nbr, h->d_desc, list, h->d_theta, h->d_exptab,
+                                h->d_u, h->d_d, acc, h->kb, h->d_pre, h->d_pre_off, jit);
+    default:
+      return bv::launch_block_v3(kind, count, b.TI, b.cap, st, h->d_pts, h->d_nbr, h->d_desc, list, h->d_theta,
+                                 h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u, h->d_d, acc, h->kb,
+                                 h->d_gslots ? h->d_gslots + b.gs_off : nullptr, h->gs_grid, h->d_pre, h->d_pre_off,
+                                 jit);
+  }
 }
 
 }  // namespace
@@ -413,7 +415,11 @@ double bv_fixed_decode(const uint64_t acc[6]) {
   return neg ? -r : r;
 }
 
-bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
+// Shared by bv_setup and the test-only bv_setup_rank_local (local = true: the
+// rank's partition is laid out exactly as under NCCL, but no communicator is
+// created and nothing is reduced across ranks).
+static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world, const void* nid, bool local,
+                            bv_handle** out) {
   if (!out) return BV_EINVAL;
   *out = nullptr;
   bv_handle* h = nullptr;
@@ -473,29 +479,25 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   }
   // sizes per position
   std::vector<int32_t> L(bc), M(bc);
-  int Nmax_all = 0;
   for (int32_t k = 0; k < bc; ++k) {
     L[k] = (int32_t)(bptr[(size_t)plan->order[k] + 1] - bptr[plan->order[k]]);
     M[k] = (int32_t)(plan->nbr_ptr[k + 1] - plan->nbr_ptr[k]);
-    Nmax_all = std::max(Nmax_all, L[k] + M[k]);
   }
-  const char* kenv = std::getenv("BV_KERNEL");  // debug/A-B only: "v1" or "v2"; default v3
-  const bool use_v1 = kenv && std::string(kenv) == "v1";
-  const bool use_v2 = kenv && std::string(kenv) == "v2";
+  // kernel choice: classic-Vecchia positions (block size 1, m ≤ 31) → warp per position
+  // (bv_cv.cu); joint sizes N ≤ 8·wmax − 1 → warp per block (bv_block_w.cu); larger →
+  // the warp-specialised CTA kernel (bv_block_v3.cu).  BV_KERNEL=v3 / BV_NO_CV=1 /
+  // BV_WMAX=t are A/B switches only.
+  const char* kenv = std::getenv("BV_KERNEL");
+  const bool force_v3 = kenv && std::string(kenv) == "v3";
+  const char* wenv = std::getenv("BV_WMAX");
+  const int wmax = force_v3 ? 0 : std::max(0, std::min(bv::w_max_ti(), wenv ? std::atoi(wenv) : 8));
   const int Nlimit = [&] {
     int N = 8;
-    if (use_v1) {
-      while (bv::v1_smem_bytes(N + 1) <= kSmemOptin) ++N;
-      return N;
-    }
     SlotTables st;
-    st.v3 = !use_v2;
     st.build(64);
     while (N + 1 < 8 * 64) {
       const int TI = (N + 1 + 8) >> 3;
-      const size_t sm = use_v2 ? bv::v2_smem_bytes(TI, st.cap[TI]) : bv::v3_smem_bytes(TI, st.cap[TI]);
-      const int mt = use_v2 ? bv::v2_maxt_for(TI) : bv::v3_maxt_for(TI);
-      if (sm > kSmemOptin || mt < 0) break;
+      if (bv::v3_smem_bytes(TI, st.cap[TI]) > kSmemOptin || bv::v3_maxt_for(TI) < 0) break;
       ++N;
     }
     return N;
@@ -505,27 +507,18 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
       return bad("position " + std::to_string(k) + " has m+l = " + std::to_string(L[k] + M[k]) +
                  " > " + std::to_string(Nlimit) + " (largest joint size this build supports)");
 
-  // distribution
-  int device = 0, rank = 0, world = 1;
-  const void* nid = nullptr;
-  if (dist) {
-    device = dist->device;
-    rank = dist->rank;
-    world = dist->world;
-    nid = dist->nccl_id;
-  }
   if (world < 1 || rank < 0 || rank >= world) return bad("invalid rank/world");
-  if (world > 1 && !nid) return bad("world > 1 needs an nccl_id");
+  if (world > 1 && !nid && !local) return bad("world > 1 needs an nccl_id");
 
   h = new bv_handle();
   h->device = device;
   h->rank = rank;
   h->world = world;
+  h->local = local;
   h->n = n;
   h->d = d;
   h->bc = bc;
-  h->use_v1 = use_v1;
-  h->use_v2 = use_v2;
+  h->wmax = wmax;
   auto bail = [&](bv_status st) {
     g_setup_err = h->err;
     release(h);
@@ -585,56 +578,53 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     const int32_t k = h->kb + q;
     desc[q] = bv::BlockDesc{pstart[k], L[k], M[k], (int32_t)(plan->nbr_ptr[k] - nb0)};
   }
-  // size buckets, largest first; inside a bucket N descending, then position.
-  //   v2: one bucket per tile-row count TI = ⌈(N+1)/8⌉;  v1: N rounded up to 16.
+  // buckets: key = TI = ⌈(N+1)/8⌉ (0 for classic-Vecchia positions, launched last);
+  // largest first, inside a bucket N descending, then position
   std::vector<int32_t> list((size_t)h->nq);
   for (int32_t q = 0; q < h->nq; ++q) list[q] = q;
   auto Nq = [&](int32_t q) { return desc[q].l + desc[q].m; };
-  // classic-Vecchia positions (block size 1, m ≤ 31: joint size ≤ 32) go to the warp-per-position
-  // kernel (bv_cv.cu) as bucket key 0 (launched last); BV_NO_CV=1 keeps them in the block kernel
   const char* nocv = std::getenv("BV_NO_CV");
-  const bool cv_ok = !use_v1 && !use_v2 && !(nocv && nocv[0] == '1');
+  const bool cv_ok = !(nocv && nocv[0] == '1');
   auto is_cv = [&](int32_t q) { return cv_ok && desc[q].l == 1 && desc[q].m <= 31; };
-  auto bkey = [&](int32_t q) {
-    return use_v1 ? (Nq(q) + kBucketWidth - 1) / kBucketWidth : is_cv(q) ? 0 : (Nq(q) + 8) >> 3;
-  };
+  auto bkey = [&](int32_t q) { return is_cv(q) ? 0 : (Nq(q) + 8) >> 3; };
   std::stable_sort(list.begin(), list.end(), [&](int32_t a, int32_t b) {
     if (bkey(a) != bkey(b)) return bkey(a) > bkey(b);
     if (Nq(a) != Nq(b)) return Nq(a) > Nq(b);
     return a < b;
   });
   SlotTables slot_tables;
-  slot_tables.v3 = !use_v2;
   int TImax_all = 1;
   for (int32_t q = 0; q < h->nq; ++q) TImax_all = std::max(TImax_all, (Nq(q) + 8) >> 3);
   slot_tables.build(TImax_all);
-  int maxN = 8;
-  size_t max_smem = 0;
-  size_t gs_total = 0;
+  h->cap_of = slot_tables.cap;
+  h->gsoff_of.assign((size_t)TImax_all + 1, 0);
+  bool any_w = false;
+  size_t max_smem = 0, gs_total = 0;
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    h->gs_grid = 2 * sms;
+  }
   for (int32_t i = 0; i < h->nq;) {
     int32_t j = i;
     while (j < h->nq && bkey(list[j]) == bkey(list[i])) ++j;
-    if (use_v1) {
-      const int Nb = std::min(Nlimit, bkey(list[i]) * kBucketWidth);
-      h->buckets.push_back(Bucket{Nb, j - i, i, 0});
-      maxN = std::max(maxN, Nb);
-    } else if (bkey(list[i]) == 0) {
-      h->buckets.push_back(Bucket{0, j - i, i, 0});  // classic-Vecchia warp kernel
+    const int TI = bkey(list[i]);
+    Bucket bk{TI, j - i, i, TI ? slot_tables.cap[TI] : 0};
+    if (TI == 0) {
+      bk.kern = kKernCV;
+    } else if (TI <= wmax) {
+      bk.kern = kKernW;
+      any_w = true;
     } else {
-      const int TI = bkey(list[i]);
-      h->buckets.push_back(Bucket{TI, j - i, i, slot_tables.cap[TI]});
-      if (!use_v2 && bv::v3_global_slots(TI)) {
-        if (h->gs_grid == 0) {
-          int sms = 148;
-          cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-          h->gs_grid = 2 * sms;
-        }
-        h->buckets.back().gs_off = gs_total;
+      bk.kern = kKernV3;
+      if (bv::v3_global_slots(TI)) {
+        bk.gs_off = gs_total;
+        h->gsoff_of[TI] = gs_total;
         gs_total += (size_t)std::min(j - i, h->gs_grid) * slot_tables.cap[TI] * 64;
       }
-      max_smem = std::max(max_smem, use_v2 ? bv::v2_smem_bytes(TI, slot_tables.cap[TI])
-                                           : bv::v3_smem_bytes(TI, slot_tables.cap[TI]));
+      max_smem = std::max(max_smem, bv::v3_smem_bytes(TI, slot_tables.cap[TI]));
     }
+    h->buckets.push_back(bk);
     i = j;
   }
 
@@ -647,13 +637,13 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   {
     // General-ν pre-generation (bv_block_v3.cu, bv_pregen_kernel): when every block's
     // packed Σ fits a small L2-resident buffer (≤ 64 MB: c1, c2), the K_ν entries are
-    // evaluated by one all-SM kernel instead of by the block kernel's update warps.
+    // evaluated by one all-SM kernel instead of inside the block kernels.
     // BV_NO_PREGEN=1 disables it (A/B and the bitwise-equality test).
     const char* npg = std::getenv("BV_NO_PREGEN");
     std::vector<int64_t> off((size_t)h->nq + 1, 0);
     for (int32_t q = 0; q < h->nq; ++q) off[(size_t)q + 1] = off[q] + (int64_t)Nq(q) * (Nq(q) + 1) / 2;
     constexpr int64_t kPreMaxBytes = 64ll << 20;
-    if (!use_v1 && !use_v2 && !(npg && npg[0] == '1') && h->nq > 0 && off[(size_t)h->nq] * 8 <= kPreMaxBytes) {
+    if (!(npg && npg[0] == '1') && h->nq > 0 && off[(size_t)h->nq] * 8 <= kPreMaxBytes) {
       TRY(upload<double>(h, &h->d_pre, nullptr, (size_t)std::max<int64_t>(1, off[(size_t)h->nq])));
       TRY(upload(h, &h->d_pre_off, off.data(), (size_t)h->nq));
       h->pre_chunks = std::max(1, std::min(64, (16 * 148 + h->nq - 1) / h->nq));
@@ -678,11 +668,10 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     for (int j = 0; j < 64; ++j) et[j] = (double)std::exp2(-(long double)j / 64.0L);
     TRY(upload(h, &h->d_exptab, et, 64));
   }
-  if (use_v1) TRYC(bv::prepare_block_v1(maxN));
-  else if (use_v2) TRYC(bv::prepare_block_v2(std::max<size_t>(max_smem, 1024)));
-  else TRYC(bv::prepare_block_v3(std::max<size_t>(max_smem, 1024)));
+  TRYC(bv::prepare_block_v3(std::max<size_t>(max_smem, 1024)));
+  if (any_w || wmax > 0) TRYC(bv::prepare_block_w());
 
-  if (world > 1) {
+  if (world > 1 && !local) {
     ncclUniqueId id;
     std::memcpy(&id, nid, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&h->comm, world, id, rank);
@@ -699,7 +688,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     TRYC(cudaStreamCreateWithFlags(&h->side[b], cudaStreamNonBlocking));
     TRYC(cudaEventCreateWithFlags(&h->join_ev[b], cudaEventDisableTiming));
   }
-  // Capture the per-evaluation graph, one per Matérn kind (the block kernel is
+  // Capture the per-evaluation graph, one per Matérn kind (the block kernels are
   // specialised on it; the kind is chosen from ν at each evaluation):
   //   θ upload → zero the accumulator → bucket kernels (largest first, spread
   //   over kBranches concurrent graph branches so small buckets overlap big
@@ -721,22 +710,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     for (int b = 0; b < nbr_streams && e == cudaSuccess; ++b) e = cudaStreamWaitEvent(h->side[b], h->fork_ev, 0);
     for (size_t bi = 0; bi < h->buckets.size() && e == cudaSuccess; ++bi) {
       const Bucket& b = h->buckets[bi];
-      cudaStream_t st = h->side[bi % nbr_streams];
-      if (use_v1)
-        e = bv::launch_block_v1(b.count, b.Nmax, st, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset,
-                                h->d_theta, h->d_u, h->d_d, h->d_acc, h->kb);
-      else if (use_v2)
-        e = bv::launch_block_v2(kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
-                                h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
-                                h->d_d, h->d_acc, h->kb);
-      else if (b.Nmax == 0)
-        e = bv::launch_cv(kind, b.count, st, h->d_pts, h->d_nbr, h->d_desc, h->d_list + b.offset, h->d_theta,
-                          h->d_exptab, h->d_u, h->d_d, h->d_acc, h->kb);
-      else
-        e = bv::launch_block_v3(pre ? 4 : kind, b.count, b.Nmax, b.cap, st, h->d_pts, h->d_nbr, h->d_desc,
-                                h->d_list + b.offset, h->d_theta, h->d_tabs, h->d_tab_off, h->d_exptab, h->d_u,
-                                h->d_d, h->d_acc, h->kb, h->d_gslots ? h->d_gslots + b.gs_off : nullptr,
-                                h->gs_grid, h->d_pre, h->d_pre_off);
+      e = launch_bucket(h, b, pre ? 4 : kind, h->side[bi % nbr_streams], h->d_list + b.offset, b.count, h->d_acc, 0.0);
     }
     for (int b = 0; b < nbr_streams && e == cudaSuccess; ++b) {
       e = cudaEventRecord(h->join_ev[b], h->side[b]);
@@ -744,7 +718,7 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
     }
     if (e == cudaSuccess) e = cudaEventRecordWithFlags(h->ev_k1, h->stream, cudaEventRecordExternal);
     ncclResult_t r = ncclSuccess;
-    if (e == cudaSuccess && world > 1)
+    if (e == cudaSuccess && h->comm)
       r = ncclAllReduce(h->d_acc, h->d_acc, 7, ncclUint64, ncclSum, h->comm, h->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(h->h_acc, h->d_acc, sizeof(unsigned long long) * bv::kAccSlots, cudaMemcpyDeviceToHost,
@@ -767,17 +741,33 @@ bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
   return BV_OK;
 }
 
+bv_status bv_setup(const bv_plan* plan, const bv_dist* dist, bv_handle** out) {
+  int device = 0, rank = 0, world = 1;
+  const void* nid = nullptr;
+  if (dist) {
+    device = dist->device;
+    rank = dist->rank;
+    world = dist->world;
+    nid = dist->nccl_id;
+  }
+  return setup_impl(plan, device, rank, world, nid, false, out);
+}
+
+bv_status bv_setup_rank_local(const bv_plan* plan, int32_t device, int32_t rank, int32_t world, bv_handle** out) {
+  return setup_impl(plan, device, rank, world, nullptr, true, out);
+}
+
 // Optional jitter mode (reading G15b; SPEC.md:197, :238 schedule with
 // base_scale = σ²): after an evaluation in which some block failed, every
-// failed position (d_k = NaN) is recomputed from scratch by the v1 kernel with
-// ε·σ² on its joint diagonal, ε = 1e-10, 1e-8, 1e-6, the first success kept.
+// failed position (d_k = NaN) is recomputed from scratch by the same block
+// kernels with ε·σ² added to every diagonal entry of its joint matrix, ε = 1e-10,
+// 1e-8, 1e-6, the first success kept — any joint size the evaluation supports.
 // The retry's exact terms go to their own accumulator and are added slot-wise
 // to the evaluation's (integer sums: still order-independent).  Collective when
 // world > 1 (every rank sees the same global failure count and enters).
 constexpr bv_status kJitterDefer = (bv_status)-1;
 static bv_status jitter_retry(bv_handle* h, const unsigned long long* acc, double* loglik) {
   static const double kSched[3] = {1e-10, 1e-8, 1e-6};
-  constexpr int kV1MaxN = 235;  // packed-lower v1 fits the 227 KB opt-in up to N = 235
   std::vector<double> dh((size_t)h->nq);
   if (h->nq > 0) BV_CUDA(h, cudaMemcpy(dh.data(), h->d_d, sizeof(double) * h->nq, cudaMemcpyDeviceToHost));
   std::vector<int32_t> F;
@@ -788,39 +778,47 @@ static bv_status jitter_retry(bv_handle* h, const unsigned long long* acc, doubl
   if (!F.empty()) {
     if (!h->d_jlist) BV_CUDA(h, cudaMalloc(&h->d_jlist, sizeof(int32_t) * (size_t)h->nq));
     if (!h->d_jacc) BV_CUDA(h, cudaMalloc(&h->d_jacc, sizeof(unsigned long long) * 9));
-    if (h->v1_ready == 0) {
-      BV_CUDA(h, bv::prepare_block_v1(kV1MaxN));
-      h->v1_ready = kV1MaxN;
-    }
     const double s2 = h->h_theta->sigma2;
-    std::vector<int32_t> keep;  // blocks too large for v1 stay failed
-    std::vector<int32_t> R;
-    for (int32_t q : F) (h->h_N[(size_t)q] <= kV1MaxN ? R : keep).push_back(q);
+    const int kind = (h->h_theta->kind == bv::kNuGeneral && h->d_pre) ? 4 : h->h_theta->kind;
+    std::vector<int32_t> R = F;
     for (int e = 0; e < 3 && !R.empty(); ++e) {
-      int Nmax = 1;
-      for (int32_t q : R) Nmax = std::max(Nmax, h->h_N[(size_t)q]);
+      // group by tile rows (the kernel family follows from TI exactly as in the evaluation)
+      auto ti = [&](int32_t q) { return (h->h_N[(size_t)q] + 8) >> 3; };
+      std::stable_sort(R.begin(), R.end(), [&](int32_t a, int32_t b) { return ti(a) < ti(b); });
       unsigned long long a0[bv::kAccSlots] = {0, 0, 0, 0, 0, 0, 0, ~0ull};
       BV_CUDA(h, cudaMemcpyAsync(h->d_jacc, a0, sizeof(a0), cudaMemcpyHostToDevice, h->stream));
       BV_CUDA(h, cudaMemcpyAsync(h->d_jlist, R.data(), sizeof(int32_t) * R.size(), cudaMemcpyHostToDevice,
                                  h->stream));
-      BV_CUDA(h, bv::launch_block_v1((int)R.size(), Nmax, h->stream, h->d_pts, h->d_nbr, h->d_desc, h->d_jlist,
-                                     h->d_theta, h->d_u, h->d_d, h->d_jacc, h->kb, kSched[e] * s2));
+      for (size_t i = 0; i < R.size();) {
+        size_t j = i;
+        while (j < R.size() && ti(R[j]) == ti(R[i])) ++j;
+        const int TI = ti(R[i]);
+        Bucket b{TI, (int)(j - i), 0, h->cap_of[(size_t)TI]};
+        b.kern = TI <= h->wmax ? kKernW : kKernV3;
+        b.gs_off = h->gsoff_of[(size_t)TI];
+        BV_CUDA(h, launch_bucket(h, b, kind, h->stream, h->d_jlist + i, b.count, h->d_jacc, kSched[e] * s2));
+        i = j;
+      }
       BV_CUDA(h, cudaMemcpyAsync(a0, h->d_jacc, sizeof(a0), cudaMemcpyDeviceToHost, h->stream));
       BV_CUDA(h, cudaMemcpyAsync(dh.data(), h->d_d, sizeof(double) * h->nq, cudaMemcpyDeviceToHost, h->stream));
       BV_CUDA(h, cudaStreamSynchronize(h->stream));
-      for (int i = 0; i < 6; ++i) sums[i] += a0[i];
       std::vector<int32_t> R2;
       for (int32_t q : R)
         if (std::isnan(dh[(size_t)q])) R2.push_back(q);
+      if (a0[6] > R2.size()) {  // a retried block became PD but its term is out of the exact range
+        h->failed_pos = (int32_t)(a0[7] >> 8);
+        *loglik = -INFINITY;
+        return fail(h, BV_EINVAL, "block term at position " + std::to_string(h->failed_pos) + " exceeds 2^96");
+      }
+      for (int i = 0; i < 6; ++i) sums[i] += a0[i];
       sums[7] += R.size() - R2.size();
       R.swap(R2);
     }
-    keep.insert(keep.end(), R.begin(), R.end());
-    F.swap(keep);
+    F.swap(R);
     sums[6] = F.size();
   }
   sums[8] = nan_local;
-  if (h->world > 1) {
+  if (h->comm) {
     if (!h->d_jacc) BV_CUDA(h, cudaMalloc(&h->d_jacc, sizeof(unsigned long long) * 9));
     BV_CUDA(h, cudaMemcpyAsync(h->d_jacc, sums, sizeof(sums), cudaMemcpyHostToDevice, h->stream));
     BV_NCCL(h, ncclAllReduce(h->d_jacc, h->d_jacc, 9, ncclUint64, ncclSum, h->comm, h->stream));
@@ -831,7 +829,7 @@ static bv_status jitter_retry(bv_handle* h, const unsigned long long* acc, doubl
   h->jitter_events = (int64_t)sums[7];
   if (sums[6] != 0) {
     unsigned long long mn = F.empty() ? ~0ull : ((unsigned long long)(h->kb + *std::min_element(F.begin(), F.end())));
-    if (h->world > 1) {
+    if (h->comm) {
       BV_CUDA(h, cudaMemcpyAsync(h->d_min, &mn, 8, cudaMemcpyHostToDevice, h->stream));
       BV_NCCL(h, ncclAllReduce(h->d_min, h->d_min, 1, ncclUint64, ncclMin, h->comm, h->stream));
       BV_CUDA(h, cudaMemcpyAsync(&mn, h->d_min, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -844,6 +842,9 @@ static bv_status jitter_retry(bv_handle* h, const unsigned long long* acc, doubl
   }
   uint64_t a6[6];
   for (int i = 0; i < 6; ++i) a6[i] = acc[i] + sums[i];
+  for (int i = 0; i < 6; ++i) h->h_acc[i] = a6[i];  // bv_loglik_acc reports the jittered sum
+  h->h_acc[6] = 0;
+  h->h_acc[7] = ~0ull;
   *loglik = bv_fixed_decode(a6);
   return BV_OK;
 }
@@ -853,7 +854,7 @@ static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
   h->jitter_events = 0;
   h->err.clear();
   if (!theta || !loglik) return fail(h, BV_EINVAL, "NULL argument");
-  if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
+  if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta: sigma2, beta must be finite and > 0; nu in {0.5, 1.5, 2.5} or [0.2, 3]");
   BV_CUDA(h, cudaSetDevice(h->device));
   fill_theta_buf(h->h_theta, h->d_theta, theta);
   h->last_kind = h->h_theta->kind;
@@ -866,7 +867,7 @@ static bv_status run_eval(bv_handle* h, const double theta[3], double* loglik) {
   }
   if (acc[6] != 0) {
     unsigned long long mn = acc[7];
-    if (h->world > 1) {
+    if (h->comm) {
       BV_CUDA(h, cudaMemcpyAsync(h->d_min, &mn, 8, cudaMemcpyHostToDevice, h->stream));
       BV_NCCL(h, ncclAllReduce(h->d_min, h->d_min, 1, ncclUint64, ncclMin, h->comm, h->stream));
       BV_CUDA(h, cudaMemcpyAsync(&mn, h->d_min, 8, cudaMemcpyDeviceToHost, h->stream));
@@ -900,8 +901,19 @@ bv_status bv_loglik_terms(bv_handle* h, const double theta[3], double* loglik, d
   return st;
 }
 
+bv_status bv_loglik_acc(bv_handle* h, const double theta[3], uint64_t acc_out[8]) {
+  if (!h || !acc_out) return BV_EINVAL;
+  double ll = 0.0;
+  const bv_status st = run_eval(h, theta, &ll);
+  if (st != BV_OK && st != BV_ENOTPD) return st;
+  for (int i = 0; i < bv::kAccSlots; ++i) acc_out[i] = h->h_acc[i];
+  return st;
+}
+
 bv_status bv_loglik_host_y(bv_handle* h, const double* y, const double theta[3], double* loglik) {
   if (!h || !y) return BV_EINVAL;
+  for (int64_t i = 0; i < h->n; ++i)
+    if (!std::isfinite(y[i])) return fail(h, BV_EINVAL, "y[" + std::to_string(i) + "] is not finite");
   BV_CUDA(h, cudaSetDevice(h->device));
   BV_CUDA(h, cudaMemcpyAsync(h->d_y_stage, y, sizeof(double) * h->n, cudaMemcpyHostToDevice, h->stream));
   BV_CUDA(h, bv::launch_scatter_y(h->d_y_stage, h->d_perm_of_id, h->n, h->d_pts, h->stream));
@@ -941,7 +953,6 @@ bv_status bv_last_error(const bv_handle* h, int32_t* failed_position, const char
 void* bv_stream(const bv_handle* h) { return h ? (void*)h->stream : nullptr; }
 
 // Debug builds only (-DBV_PROFILE_PHASES, libbv_prof.so): per-phase cycle sums.
-int bv_debug_phase_cycles(unsigned long long* out8, int reset) { return bv::debug_phase_cycles(out8, reset); }
 int bv_debug_v3_cycles(unsigned long long* out16, int reset) { return bv::debug_v3_cycles(out16, reset); }
 
 bv_status bv_last_kernel_ms(const bv_handle* h, float* ms) {
@@ -974,7 +985,7 @@ bv_status bv_predict(bv_handle* h, const double theta[3], const bv_pred_plan* pp
   h->failed_pos = -1;
   h->err.clear();
   if (!theta || !pp || !mean) return fail(h, BV_EINVAL, "NULL argument");
-  if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta must be finite and > 0");
+  if (!theta_valid(theta)) return fail(h, BV_EINVAL, "theta: sigma2, beta must be finite and > 0; nu in {0.5, 1.5, 2.5} or [0.2, 3]");
   const int64_t nn = pp->n_new;
   const int32_t bc = pp->bc_new;
   const int d = h->d;

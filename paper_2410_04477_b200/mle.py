@@ -25,6 +25,8 @@ import time
 
 import numpy as np
 
+NOT_PD = 3  # BV_ENOTPD (include/bv.h); the oracle reports non-PD with the same status
+
 THETA0 = (0.5, 0.1, 1.0)
 BOUNDS = ((0.05, 5.0), (0.005, 0.5), (0.2, 3.0))
 
@@ -48,8 +50,8 @@ def fit(loglik, theta0=THETA0, bounds=BOUNDS, max_evals: int = 2000, rtol: float
         th = to_theta(x)
         try:
             v = loglik(th)
-        except Exception as e:  # NOT_PD (a status-coded library error) → −∞; anything else is a bug
-            if not hasattr(e, "status"):
+        except Exception as e:  # NOT_PD (status 3 in the library and the oracle alike) → −∞;
+            if getattr(e, "status", None) != NOT_PD:  # any other status (EINVAL, ECUDA, ENCCL, ...) is raised
                 raise
             v = -math.inf
         trace.append((th, v))

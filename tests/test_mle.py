@@ -63,6 +63,15 @@ def test_mle_not_pd_scores_minus_inf():
     with pytest.raises(KeyError):
         fit(bad, max_evals=10)
 
+    class Cuda(RuntimeError):  # a status other than NOT_PD (here BV_ECUDA = 5) is not "infeasible θ"
+        status = 5
+
+    def broken(th):
+        raise Cuda("illegal address")
+
+    with pytest.raises(Cuda):
+        fit(broken, max_evals=10)
+
 
 @pytest.mark.gpu
 def test_mle_gpu_matches_oracle_path():
