@@ -69,6 +69,11 @@ def lib():
                                        C.c_int, C.c_int, C.c_int32, C.c_int32,
                                        C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
                                        C.POINTER(C.c_int32), C.c_uint32]
+            L.or_bv_loglik_joint.restype = C.c_int
+            L.or_bv_loglik_joint.argtypes = [C.c_int64, C.c_int, _d, _d, C.c_int32, _i32, _i32, _i64, _i32, _d,
+                                             C.c_int, C.c_int, C.c_int32, C.c_int32,
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
+                                             C.POINTER(C.c_int32)]
             L.or_bv_loglik_jitter.restype = C.c_int
             L.or_bv_loglik_jitter.argtypes = [C.c_int64, C.c_int, _d, _d, C.c_int32, _i32, _i32, _i64, _i32, _d,
                                               C.c_int, C.c_int32, C.c_int32, _d, _d, _d, _d,
@@ -165,6 +170,26 @@ def bv_loglik(plan, theta, long_double: bool = False, nthreads: int = 0, k_range
                         1 if long_double else 0, int(nthreads), kb, ke,
                         u.ctypes.data if per_block else None, dd.ctypes.data if per_block else None,
                         t.ctypes.data if per_block else None, C.byref(ll), C.byref(fp), int(perturb_seed))
+    if st:
+        raise OracleError(st, fp.value)
+    return {"loglik": ll.value, "u": u, "d": dd, "t": t}
+
+
+def bv_loglik_joint(plan, theta, long_double: bool = False, nthreads: int = 0):
+    """DIAGNOSTIC ONLY (not a parity reference): the block terms through the joint-Cholesky
+    formulation (or_bv_loglik_joint), to measure how far two exact FP64 formulations of Alg. 1
+    differ on ill-conditioned blocks (tools/parity_diag.py, reading G22)."""
+    L = lib()
+    locs = _c(plan.locs, np.float64)
+    n, d = locs.shape
+    bc = int(plan.order.shape[0])
+    u, dd, t = np.zeros(bc), np.zeros(bc), np.zeros(bc)
+    ll = C.c_double(0.0)
+    fp = C.c_int32(-1)
+    st = L.or_bv_loglik_joint(n, d, locs, _c(plan.y, np.float64), bc, _c(plan.block_id, np.int32),
+                              _c(plan.order, np.int32), _c(plan.nbr_ptr, np.int64), _c(plan.nbr_idx, np.int32),
+                              _c(theta, np.float64), 1 if long_double else 0, int(nthreads), 0, bc, u.ctypes.data,
+                              dd.ctypes.data, t.ctypes.data, C.byref(ll), C.byref(fp))
     if st:
         raise OracleError(st, fp.value)
     return {"loglik": ll.value, "u": u, "d": dd, "t": t}

@@ -266,11 +266,51 @@ int alg1_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R
   return 0;
 }
 
+/* DIAGNOSTIC ONLY (not a parity reference): the same block term through the
+ * other exact formulation — ONE unblocked right-looking Cholesky of the joint
+ * (N+1)×(N+1) matrix [[Σcon, Σcross, ·],[Σcrossᵀ, Σlk, ·],[y_NNᵀ, y_Bᵀ, ·]]
+ * (neighbours first, the y row appended and eliminated but never pivoted):
+ * d = Σ_{j≥m} log p_j, u = Σ_{j≥m} L_Nj² (identical to l.17-27 in exact
+ * arithmetic).  Lets tools/parity_diag.py measure how far two
+ * FP64 formulations of Alg. 1 differ on ill-conditioned blocks (reading G22). */
+template <class R>
+int joint_block(const PlanView& P, int32_t k, R sigma2, R beta, R nu, R* u_out, R* d_out) {
+  const int32_t b = P.order[k];
+  const int l = (int)(P.bptr[(size_t)b + 1] - P.bptr[b]);
+  const int32_t* B = P.bidx.data() + P.bptr[b];
+  const int m = (int)(P.nbr_ptr[(size_t)k + 1] - P.nbr_ptr[k]);
+  const int32_t* NN = P.nbr_idx + P.nbr_ptr[k];
+  const int N = m + l, d = P.d;
+  std::vector<int32_t> id((size_t)N);
+  for (int a = 0; a < m; ++a) id[a] = NN[a];
+  for (int a = 0; a < l; ++a) id[(size_t)m + a] = B[a];
+  auto loc = [&](int32_t i) { return P.locs + (size_t)i * d; };
+  const int Na = N + 1;
+  std::vector<R> A((size_t)Na * Na, R(0));  // lower triangle, row-major
+  for (int r = 0; r < N; ++r)
+    for (int c = 0; c <= r; ++c) A[(size_t)r * Na + c] = matern<R>(dist<R>(loc(id[r]), loc(id[c]), d), sigma2, beta, nu);
+  for (int c = 0; c < N; ++c) A[(size_t)N * Na + c] = R(P.y[id[c]]);
+  R u = 0, ld = 0;
+  for (int j = 0; j < N; ++j) {
+    const R p = A[(size_t)j * Na + j];
+    if (!(p > R(kPivotFloor) * sigma2) || !std::isfinite((double)p)) return 3;
+    const R Ljj = std::sqrt(p);
+    if (j >= m) ld += std::log(p);
+    for (int i = j + 1; i <= N; ++i) A[(size_t)i * Na + j] /= Ljj;
+    for (int i = j + 1; i <= N; ++i)
+      for (int c = j + 1; c <= i && c < N; ++c) A[(size_t)i * Na + c] -= A[(size_t)i * Na + j] * A[(size_t)c * Na + j];
+    if (j >= m) u += A[(size_t)N * Na + j] * A[(size_t)N * Na + j];
+  }
+  *u_out = u;
+  *d_out = ld;
+  return 0;
+}
+
 template <class R>
 int bv_loglik_impl(PlanView& P, const int32_t* block_id, const double* theta, double* out_u, double* out_d,
                    double* out_t, double* out_loglik, int32_t* failed_pos, int nthreads, int k_begin, int k_end,
                    double* out_loglik_ld_sum, uint32_t seed, int jitter_mode = 0, double* out_eps = nullptr,
-                   int32_t* out_events = nullptr) {
+                   int32_t* out_events = nullptr, int joint = 0) {
   build_block_lists(P, block_id);
   const R sigma2 = R(theta[0]), beta = R(theta[1]), nu = R(theta[2]);
   const int nk = k_end - k_begin;
@@ -283,7 +323,7 @@ int bv_loglik_impl(PlanView& P, const int32_t* block_id, const double* theta, do
   for (int q = 0; q < nk; ++q) {
     const int32_t k = k_begin + q;
     R u = 0, d = 0;
-    st[q] = alg1_block<R>(P, k, sigma2, beta, nu, &u, &d, seed);
+    st[q] = joint ? joint_block<R>(P, k, sigma2, beta, nu, &u, &d) : alg1_block<R>(P, k, sigma2, beta, nu, &u, &d, seed);
     // Optional jitter mode (reading G15b; SPEC.md:197 schedule with base_scale = σ²,
     // SPEC.md:238): a block whose POTRF failed is re-run from scratch with
     // ε·σ² added to every diagonal entry of Σcon and Σlk, ε = 1e-10, 1e-8, 1e-6
@@ -415,6 +455,22 @@ int or_bv_loglik(int64_t n, int d, const double* locs, const double* y, int32_t 
                                        k_begin, k_end, nullptr, 0u);
   return bv_loglik_impl<double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads, k_begin,
                                 k_end, nullptr, perturb_seed);
+}
+
+/* DIAGNOSTIC ONLY: or_bv_loglik through the joint formulation (joint_block above);
+ * same arguments minus perturb_seed.  Not used for parity. */
+int or_bv_loglik_joint(int64_t n, int d, const double* locs, const double* y, int32_t bc, const int32_t* block_id,
+                       const int32_t* order, const int64_t* nbr_ptr, const int32_t* nbr_idx, const double* theta,
+                       int long_double, int nthreads, int32_t k_begin, int32_t k_end, double* out_u, double* out_d,
+                       double* out_t, double* out_loglik, int32_t* failed_pos) {
+  if (!theta_ok(theta) || n < 1 || (d != 2 && d != 3) || bc < 1 || k_begin < 0 || k_end > bc || k_begin > k_end)
+    return 2;
+  PlanView P{n, d, locs, y, bc, order, nbr_ptr, nbr_idx, {}, {}};
+  if (long_double)
+    return bv_loglik_impl<long double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads,
+                                       k_begin, k_end, nullptr, 0u, 0, nullptr, nullptr, 1);
+  return bv_loglik_impl<double>(P, block_id, theta, out_u, out_d, out_t, out_loglik, failed_pos, nthreads, k_begin,
+                                k_end, nullptr, 0u, 0, nullptr, nullptr, 1);
 }
 
 /* Alg. 1 with the optional jitter mode (reading G15b): per block, the

@@ -42,7 +42,7 @@ namespace v3 {
 // 187/180/166 evals/s against 197 (round 1).
 constexpr int kW = 4;  // warps per CTA: 1 chain warp + kW−1 update warps
 constexpr int kNT = kW * 32;
-constexpr int kBarG = 1, kBarF = 2, kBarE = 3, kBarU = 4, kBarH = 5;  // named barriers (0 = __syncthreads)
+constexpr int kBarG = 1, kBarF = 2, kBarE = 3, kBarH = 5;  // named barriers (0 = __syncthreads)
 
 #ifdef BV_PROFILE_PHASES
 // Debug-only phase timers, summed over warps (lane 0): chain 0 factor, 1 wait E,
@@ -115,10 +115,15 @@ __device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec
 
 // In-lane Cholesky of the 8×8 tile t (row-major lower, every lane holds it),
 // then L_JJ⁻¹ by columns (lane j solves L x = e_j).  Lanes 0..7 publish column
-// j of both L_JJ (lf) and L_JJ⁻¹ (li) in DMMA fragment order: element (i,k) at
-// 2(4i + (k&3)) + (k>>2).  Padding pivots (j ≥ N − 8J) get 1/L_jj = 0, so
-// their rows of L_JJ⁻¹ — and with them the padding columns of every
-// L(I,J) = C(I,J) L_JJ⁻ᵀ — are zero.
+// j of L_JJ⁻¹ (li), lane 0 all of L_JJ (lf), both in DMMA fragment order:
+// element (i,k) at 2(4i + (k&3)) + (k>>2).  The pivot chain carries no selects:
+// padding rows are far points (pivot σ², exactly zero coupling, so their rows
+// and columns of L_JJ and L_JJ⁻¹ are exactly decoupled and the padding columns
+// of every L(I,J) = C(I,J) L_JJ⁻ᵀ stay zero); the y row's "pivot" (eliminated,
+// never pivoted) only poisons rows below it in the LAST tile, which no solve
+// reads.  Pivot checks (reading G15) and the d product over real rows j ≥ m
+// run on the recorded pivots, off the chain.  jit: the optional jitter mode's
+// ε·σ² on the diagonal (reading G15b; harmless on padding and the y row).
 __device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, int J, int m, int N, int lane,
                                             double pfloor, double jit, double& prod, int& nbad, double& qd) {
   const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
@@ -127,26 +132,24 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int k = 0; k <= i; ++k) a[i][k] = t[8 * i + k];
-  // optional jitter mode (reading G15b): ε·σ² on every real diagonal entry of the joint matrix
 #pragma unroll
-  for (int i = 0; i < 8; ++i) a[i][i] += (i < nreal) ? jit : 0.0;
+  for (int i = 0; i < 8; ++i) a[i][i] += jit;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    double p = a[j][j];
-    const bool ok = (p > pfloor) & (p <= 1.7976931348623157e308);  // reading G15
-    const bool real = j < nreal;
-    nbad += (real & !ok) ? 1 : 0;
-    p = (real & ok) ? p : 1.0;
-    prod *= (j >= jm) ? p : 1.0;
+    const double p = a[j][j];
     const double r = rsqrt_pos(p);
-    const double rv = real ? r : 0.0;
     const double lv = p * r;
-    rr[j] = rv;
+    {  // off the chain: pivot check (reading G15) and the d product over real rows ≥ m
+      const bool real = j < nreal, ok = (p > pfloor) & (p <= 1.7976931348623157e308);
+      nbad += (real & !ok) ? 1 : 0;
+      prod *= (real & (j >= jm)) ? p : 1.0;
+    }
+    rr[j] = r;
     a[j][j] = lv;
 #pragma unroll
     for (int i = j + 1; i < 8; ++i) {
-      const double x = a[i][j] * rv;
-      a[i][j] = fma(fma(-x, lv, a[i][j]), rv, x);
+      const double x = a[i][j] * r;
+      a[i][j] = fma(fma(-x, lv, a[i][j]), r, x);
     }
 #pragma unroll
     for (int i = j + 1; i < 8; ++i)
@@ -172,14 +175,13 @@ __device__ __forceinline__ void factor_tile(const double* t, double* lf, double*
   }
   if (lane < 8) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int o = 2 * (4 * i + (j & 3)) + (j >> 2);
-      li[o] = x[i];
-      double l = 0.0;
+    for (int i = 0; i < 8; ++i) li[2 * (4 * i + (j & 3)) + (j >> 2)] = x[i];
+  }
+  if (lane == 0) {
 #pragma unroll
-      for (int k = 0; k <= i; ++k) l = (k == j) ? a[i][k] : l;
-      lf[o] = l;
-    }
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) sts2(lf + 2 * (4 * i + k), k <= i ? a[i][k] : 0.0, k + 4 <= i ? a[i][k + 4] : 0.0);
   }
 }
 
@@ -256,9 +258,35 @@ __device__ __forceinline__ double* slot_at(double* base, unsigned slot) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(base) + (slot << 9));
 }
 
-template <int NS, int MAXT>
-__device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
-                                       int uw, int lane) {
+// Update-warp column work for NS tiles I = J+uw+3s of column J+1 (warp 1's first
+// tile is the next diagonal tile): generate A(I,J+1) (Eq. 7) straight into the
+// MMA accumulators (lane (g,t): row g, columns 2t, 2t+1), then subtract the
+// updates of panels K < J progressively, S ← S − L(I,K) L(J+1,K)ᵀ in increasing
+// K — the rounding order of a right-looking elimination (each update rounds
+// against the partially reduced value, not against the full sum of updates),
+// which on ill-conditioned blocks is several times more accurate than summing
+// the updates and subtracting once.
+template <int NS, int MAXT, int KIND>
+__device__ __forceinline__ void u_column(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
+                                         int uw, int lane, const PointRec* P, int N, const Theta& th,
+                                         const double* etab, const double* pre) {
+  const int g = lane >> 2, t = lane & 3, c0 = 8 * (J + 1) + 2 * t;
+  const PointRec pc0 = P[c0], pc1 = P[c0 + 1];
+  // one tile at a time (a runtime loop, the result placed by a compile-time select): the
+  // Matérn temporaries of one tile in flight, not of all NS, keep the 102-register budget
+#pragma unroll 1
+  for (int s = 0; s < NS; ++s) {
+    const int r = 8 * (J + uw + (kW - 1) * s) + g;
+    const PointRec pr = P[r];
+    const double v0 = joint_entry<KIND>(pr, pc0, r, c0, N, th, etab, pre);
+    const double v1 = joint_entry<KIND>(pr, pc1, r, c0 + 1, N, th, etab, pre);
+#pragma unroll
+    for (int q = 0; q < NS; ++q)
+      if (q == s) {
+        S[q][0] = v0;
+        S[q][1] = v1;
+      }
+  }
   // slot s of this lane's fragment pair: one shift-add from an unsigned 16-bit slot index
   const double* sl = slots + 2 * lane;
   const uint16_t* tJ = reinterpret_cast<const uint16_t*>(tab) + (J + 1) * TI;
@@ -268,18 +296,17 @@ __device__ __forceinline__ void u_gemm(double (&S)[MAXT][2], const double* slots
 #pragma unroll 2
   for (int K = 0; K < J; ++K) {
     const double2 b = lds2(slot_at(sl, tJ[K]));
+    const double bx = neg(b.x), by = neg(b.y);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       const double2 a = lds2(slot_at(sl, tI[s][K]));
-      dmma884(S[s][0], S[s][1], a.x, b.x);
-      dmma884(S[s][0], S[s][1], a.y, b.y);
+      dmma884(S[s][0], S[s][1], a.x, bx);
+      dmma884(S[s][0], S[s][1], a.y, by);
     }
   }
 }
 
 
-// One half-tile of generation in flight per update warp (two measured the same, round 1).
-constexpr int kV3GenUnroll = 1;
 
 // CTAs per SM the register allocation targets: shared memory admits 5 blocks
 // of TI ≤ 16 (MAXT ≤ 5, the bulk of c3/c4) and 4 of TI 17-18; 5 × 128 threads
@@ -436,48 +463,22 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
 #pragma unroll
       for (int s = 0; s < MAXT; ++s) S[s][0] = S[s][1] = 0.0;
       if (ahead) {
-        P3_T(u5);
-        // a3: A(I,J+1), I ≥ J+1 (the diagonal one into ptile, the rest into
-        // their slots), by half-tiles h (rows 4(h&1)..+3 of tile I = J+1+h/2)
-        // dealt round-robin to the update warps.  A lane's column c is fixed,
-        // so its point, its validity and its in-tile offset are loop-invariant;
-        // a half-tile is 32 consecutive doubles of the row-major tile.
-        {
-          const int c = 8 * (J + 1) + (lane & 7);
-          const PointRec pc = P[c];
-          const int nh = 2 * (TI - J - 1);
-          const int r0 = 8 * (J + 1) + (lane >> 3);  // half-tile h covers rows r0 + 4h (+ lane/8)
-#pragma unroll(kV3GenUnroll)
-          for (int h = uw - 1; h < nh; h += kW - 1) {
-            const int I = J + 1 + (h >> 1), r = r0 + 4 * h;
-            double v;
-            if constexpr (KIND == kPre) v = pre_entry(preb, r, c, N, th.sigma2);
-            else v = matern_kind<KIND>(sqdist(P[r], pc), th, etab);
-            v = (r == N) ? pc.v : v;  // padding entries are 0 by construction (far points)
-            double* dst = (h < 2) ? ptile : slot_at(slots, tabu[I * TI + J + 1]);
-            dst[32 * (h & 1) + lane] = v;
-          }
-        }
-        P3_ADD(5, u5);
         P3_T(u6);
-        // partial update of this warp's tiles I = J+1+(u−1)+3s (exact count)
+        // a3 + a6: this warp's tiles of column J+1, generated into registers and reduced by
+        // the panels K < J (exact tile count per warp: no predicated-off work)
         const int ns = (TI - J - 1 - (uw - 1) + (kW - 2)) / (kW - 1);
         switch (ns) {
-#define BV_NS(n) \
-  case n:        \
-    if (MAXT >= n) u_gemm<(MAXT >= n ? n : 1), MAXT>(S, slots, tab, TI, J, uw, lane); \
+#define BV_NS(n)                                                                                              \
+  case n:                                                                                                     \
+    if (MAXT >= n) u_column<(MAXT >= n ? n : 1), MAXT, KIND>(S, slots, tab, TI, J, uw, lane, P, N, th, etab, preb); \
     break;
           BV_NS(1) BV_NS(2) BV_NS(3) BV_NS(4) BV_NS(5) BV_NS(6) BV_NS(7) BV_NS(8) BV_NS(9) BV_NS(10) BV_NS(11)
           BV_NS(12) BV_NS(13) BV_NS(14) BV_NS(15) BV_NS(16) BV_NS(17) BV_NS(18) BV_NS(19) BV_NS(20)
 #undef BV_NS
           default: break;
         }
-        bar_sync(kBarU, (kW - 1) * 32);  // ptile generated by all update threads
-        if (uw == 1) {        // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp
-          double* pp = ptile + 8 * g + 2 * t;
-          const double2 av = lds2(pp);
-          sts2(pp, av.x - S[0][0], av.y - S[0][1]);
-        }
+        // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp (warp 1 owns the tile)
+        if (uw == 1) sts2(ptile + 8 * g + 2 * t, S[0][0], S[0][1]);
         P3_ADD(6, u6);
       }
       P3_T(u7);
@@ -519,11 +520,9 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         const int I = J + uw + (kW - 1) * s;
         if (I < TI && I > J + 1) {  // the diagonal tile's last term is the chain warp's
           const double2 a = lds2(slot_at(slots + 2 * lane, tabu[I * TI + J]));
-          dmma884(S[s][0], S[s][1], a.x, b.x);
-          dmma884(S[s][0], S[s][1], a.y, b.y);
-          double* cp = slot_at(slots + 8 * g + 2 * t, tabu[I * TI + J + 1]);
-          const double2 av = lds2(cp);
-          sts2(cp, av.x - S[s][0], av.y - S[s][1]);
+          dmma884(S[s][0], S[s][1], a.x, neg(b.x));
+          dmma884(S[s][0], S[s][1], a.y, neg(b.y));
+          sts2(slot_at(slots + 8 * g + 2 * t, tabu[I * TI + J + 1]), S[s][0], S[s][1]);  // C(I,J+1), row-major
         }
       }
       __syncwarp();

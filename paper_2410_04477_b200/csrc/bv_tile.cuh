@@ -97,7 +97,7 @@ template <bool NEGIN>
 __device__ __forceinline__ void factor_tile(const double* dg, double* lb, double* zb, int J, int m, int N, int lane,
                                             double pfloor, double jit, double& prod, int& nbad, double& qd) {
   const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
-  double a[8][8], rr[8], pv[8];
+  double a[8][8], rr[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -109,7 +109,11 @@ __device__ __forceinline__ void factor_tile(const double* dg, double* lb, double
     const double p = a[j][j];
     const double r = rsqrt_pos(p);
     const double lv = p * r;
-    pv[j] = p;
+    {  // off the chain: pivot check (reading G15) and the d product over real rows ≥ m
+      const bool real = j < nreal, ok = (p > pfloor) & (p <= 1.7976931348623157e308);
+      nbad += (real & !ok) ? 1 : 0;
+      prod *= (real & (j >= jm)) ? p : 1.0;
+    }
     rr[j] = r;
     a[j][j] = lv;
 #pragma unroll
@@ -121,13 +125,6 @@ __device__ __forceinline__ void factor_tile(const double* dg, double* lb, double
     for (int i = j + 1; i < 8; ++i)
 #pragma unroll
       for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
-  }
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const bool real = j < nreal;
-    const bool ok = (pv[j] > pfloor) & (pv[j] <= 1.7976931348623157e308);
-    nbad += (real & !ok) ? 1 : 0;
-    prod *= (real & (j >= jm)) ? pv[j] : 1.0;
   }
 #pragma unroll
   for (int i = 1; i < 8; ++i)

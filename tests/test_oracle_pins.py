@@ -400,3 +400,17 @@ def test_jitter_mode_is_identity_without_failures():
     b = oracle.bv_loglik_jitter(p, theta)
     assert b["events"] == 0 and not b["eps"].any()
     assert a["loglik"] == b["loglik"] and np.array_equal(a["t"], b["t"])
+
+
+def test_joint_formulation_diagnostic_agrees_in_long_double():
+    """The diagnostic joint-Cholesky formulation (oracle.bv_loglik_joint, used only by
+    tools/parity_diag.py) is exact arithmetic's same quantity: in 80-bit it equals Alg. 1 literal
+    to rounding; in FP64 it differs by the formulation's own rounding."""
+    theta = (1.0, 0.09, 1.5)
+    p = bvgen.make_plan("c1", n=600, bc=12, m=24, cfg=41)
+    p = p.with_y(oracle.simulate_bv(p, theta, bvgen.normal(4102, p.n)))
+    a = oracle.bv_loglik(p, theta, long_double=True)
+    b = oracle.bv_loglik_joint(p, theta, long_double=True)
+    sc = np.abs(a["u"]) + np.abs(a["d"]) + 1.0
+    assert np.max(np.abs(a["u"] - b["u"]) / sc) < 1e-13 and np.max(np.abs(a["d"] - b["d"]) / sc) < 1e-13
+    assert abs(a["loglik"] - b["loglik"]) <= 1e-13 * abs(a["loglik"])
