@@ -1,8 +1,9 @@
 """CPU oracle for the block-Vecchia log-likelihood (arXiv 2410.04477).
 
-TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
-``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
-package.  It shares no code with the CUDA product path
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()``,
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs and the offline
+diagnostics under ``tools/`` (parity_diag, pivot_floor_audit, accuracy_c5) may
+import this package.  It shares no code with the CUDA product path
 (``paper_2410_04477_b200``) and never imports it.
 
 The arithmetic lives in ``bv_oracle.cpp`` (plain C++17 loops, FP64 and x87
@@ -173,6 +174,15 @@ def bv_loglik(plan, theta, long_double: bool = False, nthreads: int = 0, k_range
     if st:
         raise OracleError(st, fp.value)
     return {"loglik": ll.value, "u": u, "d": dd, "t": t}
+
+
+def set_pivot_floor(f: float = 1e-14):
+    """Reading G15's non-PD floor (a pivot must exceed f·σ²; 0 = plain "≤ 0"), process-global.
+    For the floor audit (tools/pivot_floor_audit.py); every other caller keeps the default."""
+    L = lib()
+    L.or_set_pivot_floor.argtypes = [C.c_double]
+    L.or_set_pivot_floor.restype = None
+    L.or_set_pivot_floor(float(f))
 
 
 def bv_loglik_joint(plan, theta, long_double: bool = False, nthreads: int = 0):

@@ -1,8 +1,9 @@
 /* =============================================================================
  * oracle/bv_oracle.cpp — CPU ORACLE for the block-Vecchia log-likelihood.
  *
- * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
- * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke(), bench.py's
+ * cpu_baseline / --impl reference legs and the offline diagnostics under tools/
+ * (parity_diag, pivot_floor_audit, accuracy_c5) may load this library.
  * It shares no code, header, table or constant with the CUDA product path
  * (paper_2410_04477_b200/), and it never includes anything from there.
  *
@@ -16,6 +17,11 @@
  *                        steps, NOT the fused joint Cholesky the GPU uses.
  *   or_bv_loglik_jitter  the same with the optional jitter retry schedule
  *                        (reading G15b).
+ *   or_bv_loglik_joint   DIAGNOSTIC ONLY, never a parity reference: the same
+ *                        block terms through the other exact formulation (one
+ *                        joint Cholesky), to measure how two FP64 formulations
+ *                        differ on ill-conditioned blocks (reading G22).
+ *   or_set_pivot_floor   the non-PD floor of reading G15 (floor audit only).
  *   or_exact_loglik      Eq. (1), PAPER.md:62-67 (§1) — dense Cholesky.
  *   or_classic_vecchia   classic Vecchia = block size 1, PAPER.md:76-78, :83;
  *                        univariate conditionals solved by Gaussian
@@ -26,7 +32,8 @@
  *                        from ONE joint dense Cholesky of [NN; B] (a different
  *                        formulation from or_bv_loglik, so the generating-model
  *                        pin u_i ≈ ‖ε_i‖² cross-checks two formulations).
- *   or_simulate_exact    y = chol(Σθ) ε, for exact GRFs at small n.
+ *   or_simulate_exact    y = chol(Σθ) ε, for exact GRFs at small n (pinned:
+ *                        Eq. (1) at y plus ½‖ε‖² is ε-independent).
  *   or_bv_predict        Alg. 2 l.8-13, PAPER.md:651-662 (§S1; §2.3
  *                        PAPER.md:194-240) taken literally per prediction block:
  *                        Σcon, Σcross, Σlk → L = POTRF(Σcon), W = L⁻¹Σcross,
@@ -135,7 +142,7 @@ inline long double perturb_entry(long double v, int32_t, int32_t, uint32_t) { re
  * pivots are compared with kPivotFloor·σ², σ² being every diagonal entry of
  * Σθ, so an FP64-singular matrix — e.g. a repeated location, whose pivot is
  * rounding noise of either sign — fails whatever the rounding order). */
-constexpr double kPivotFloor = 1e-14;
+double kPivotFloor = 1e-14;  // reading G15; or_set_pivot_floor changes it (the floor audit only)
 template <class R> bool potrf(const std::vector<R>& A, std::vector<R>& L, int n, R floor = R(0)) {
   L.assign((size_t)n * n, R(0));
   for (int j = 0; j < n; ++j) {
@@ -408,6 +415,11 @@ bool theta_ok(const double* th) {
 }  // namespace
 
 extern "C" {
+
+/* The non-PD floor of reading G15 (default 1e-14, i.e. a pivot must exceed 1e-14·σ²);
+ * 0 = SURVEY §8b's plain "pivot ≤ 0" rule.  Process-global; for the floor audit
+ * (tools/pivot_floor_audit.py) only. */
+void or_set_pivot_floor(double f) { kPivotFloor = f; }
 
 /* Eq. (7).  mode 0: dispatching (closed forms at ν ∈ {½,3/2,5/2});
  * mode 1: always the general K_ν path; mode 2: long-double dispatching. */

@@ -116,15 +116,24 @@ def compare_all_strict_then_ld(plan, theta, gpu_d, gpu_u, o64, label, gpu_ll=Non
     miss = np.where(e_blk > TOL_BLOCK)[0]
     assert len(miss) <= max_ld, f"{label}: {len(miss)} blocks miss 1e-10 (more than {max_ld})"
     bad, exc = [], []
+    whole = len(miss) > 100  # many misses: one whole-range 80-bit run instead of one per position
+    old_all = oracle.bv_loglik(plan, theta, long_double=True) if whole else None
+    reps_all = None
     for k in miss:
         kr = (int(k), int(k) + 1)
-        old = oracle.bv_loglik(plan, theta, long_double=True, k_range=kr)
+        old = ({n: old_all[n][k:k + 1] for n in ("d", "u", "t")} if whole else
+               oracle.bv_loglik(plan, theta, long_double=True, k_range=kr))
         reps = None
         for name, g in (("d", gpu_d[k]), ("u", gpu_u[k]), ("t", gpu_t[k])):
             delta = abs(o64[name][k] - old[name][0]) / s[k]
             eld = abs(g - old[name][0]) / s[k]
             if abs(g - o64[name][k]) / s[k] > TOL_BLOCK and not (delta > 1e-11 and eld <= 10 * delta):
-                reps = reps or [oracle.bv_loglik(plan, theta, k_range=kr, perturb_seed=2000 + q) for q in range(1, 7)]
+                if reps is None:
+                    if whole:
+                        reps_all = reps_all or [oracle.bv_loglik(plan, theta, perturb_seed=2000 + q) for q in range(1, 7)]
+                        reps = [{n: r[n][k:k + 1] for n in ("d", "u", "t")} for r in reps_all]
+                    else:
+                        reps = [oracle.bv_loglik(plan, theta, k_range=kr, perturb_seed=2000 + q) for q in range(1, 7)]
                 dr = max([delta] + [abs(r[name][0] - old[name][0]) / s[k] for r in reps])
                 (exc if (dr > 1e-11 and eld <= 10 * dr) else bad).append((int(k), name, float(delta), float(eld)))
     nbad = len({b[0] for b in bad})

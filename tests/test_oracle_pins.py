@@ -414,3 +414,21 @@ def test_joint_formulation_diagnostic_agrees_in_long_double():
     sc = np.abs(a["u"]) + np.abs(a["d"]) + 1.0
     assert np.max(np.abs(a["u"] - b["u"]) / sc) < 1e-13 and np.max(np.abs(a["d"] - b["d"]) / sc) < 1e-13
     assert abs(a["loglik"] - b["loglik"]) <= 1e-13 * abs(a["loglik"])
+
+
+def test_simulate_exact_is_the_cholesky_draw():
+    """or_simulate_exact draws y = L ε with L L ᵀ = Σ(θ): then yᵀΣ⁻¹y = ‖ε‖², so Eq. (1) at y plus
+    ½‖ε‖² is the same number −½(log|Σ| + n log 2π) for every ε (pinned against exact_loglik, itself
+    pinned by the Cholesky hand example and the bc = 1 reduction).  A wrong factor (transposed, not
+    the Cholesky of Σ) breaks the identity."""
+    theta = (1.3, 0.12, 1.5)
+    locs = bvgen.locations(77, 300, 2)
+    vals = []
+    for seed in (1, 2, 3):
+        eps = bvgen.normal(7700 + seed, 300)
+        y = oracle.simulate_exact(locs, theta, eps)
+        vals.append(oracle.exact_loglik(locs, y, theta) + 0.5 * float(eps @ eps))
+    assert max(vals) - min(vals) <= 1e-9 * abs(vals[0]), vals
+    # and y = 0·ε gives exactly that constant
+    z = oracle.exact_loglik(locs, oracle.simulate_exact(locs, theta, np.zeros(300)), theta)
+    assert abs(z - vals[0]) <= 1e-9 * abs(z)

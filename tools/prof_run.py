@@ -1,6 +1,6 @@
 """Minimal profiling target: set up one config and run a few evaluations.
 
-    python tools/prof_run.py [config] [evals]
+    python tools/prof_run.py [config] [evals] [m]
 Used under `ncu` (one GPU) to capture the block kernels; prints the per-bucket
 launch plan so the ncu launch list can be mapped back to tile sizes."""
 import os
@@ -17,7 +17,8 @@ import paper_2410_04477_b200 as bvl  # noqa: E402
 def main():
     cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
     evals = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-    plan = bvgen.cached_plan(cfg)
+    m = int(sys.argv[3]) if len(sys.argv) > 3 else None
+    plan = bvgen.cached_plan(cfg, m=m)
     l, m = plan.block_sizes()
     TI = (l + m + 8) // 8
     vals, cnts = np.unique(TI, return_counts=True)
