@@ -1,21 +1,30 @@
-// bv_block_w.cu — the small-block kernel: ONE WARP per block (joint sizes N ≤ 8·TI−1,
-// TI ≤ kWMaxTI), many blocks per SM.
+// bv_block_w.cu — the small-block kernel: ONE WARP per block, the whole joint
+// matrix in REGISTERS (joint sizes N ≤ 8·TI − 1, TI ≤ kWMaxTI), many blocks per SM.
 //
 // Same mathematics as the large-block kernel (Alg. 1 l.10-29, PAPER.md:593-632,
 // fused into one Cholesky of the joint matrix with the y row appended, DESIGN.md
 // §4), for the small conditioning sets of c5 at m = 30 (N median 49): there a
 // block's whole elimination is a few thousand FP64 MMAs, too little to split
-// across warps without the hand-offs dominating, so each warp owns one block
-// and the SM's ~12-16 resident warps (one per block) hide each other's pivot
-// chains.  No barriers beyond __syncwarp.
+// across warps, so each warp owns one block and the SM's ~12-20 resident warps
+// (one per block) hide each other's latency.
 //
-// The packed lower triangle of 8×8 tiles lives in shared memory, negated, in the
-// MMA accumulator layout (bv_tile.cuh).  Right-looking: per column panel J the
-// diagonal tile is factored in-lane (tile::factor_tile), column J is solved
-// (L(I,J) = C(I,J) L_JJ⁻ᵀ, FP64 MMA with one refinement step) and the trailing
-// tiles get Ĉ(I,K) += L(I,J) L(K,J)ᵀ.  Solves and updates run in batches of
-// four independent tiles (loads, then MMAs, then stores) so their MMA latency
-// chains overlap.
+// The tiles live in registers, negated (Ĉ = −C), one double2 per lane per tile in
+// the MMA accumulator layout (bv_tile.cuh): lane (g,t) holds row g, columns 2t and
+// 2t+1.  Left-looking over the column panels K (all compile-time: TI is a template
+// parameter, the panel loop is unrolled, so every tile index and every MMA is
+// static and nothing is predicated), per panel:
+//   generate A(I,K), I ≥ K (Eq. 7; a compact loop staged through shared memory,
+//     then into registers);
+//   Ĉ(I,K) += L(I,K') L(K,K')ᵀ for K' = 0..K−1 in that order — progressive
+//     subtraction, the rounding order of a right-looking elimination;
+//   factor Ĉ(K,K) across the warp's lanes (factor_dist below: the pivot, the scaled
+//     column and the inverse's rows move by shuffles — no 32-lane redundant in-lane
+//     factorisation); L_KK and −L_KK⁻¹ come out already in the B-fragment form;
+//   L(I,K) = C(I,K) L_KK⁻ᵀ for I > K (tile::trsm: explicit inverse + one FP64
+//     refinement step).
+// Only the L tiles still to be read (rows ≥ K of the panels < K) and panel K are
+// live: ≈ (TI/2)² + TI tiles instead of TI(TI+1)/2, which keeps the register file
+// at 16+ resident blocks per SM.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,161 +34,177 @@ namespace bv {
 namespace wk {
 
 using namespace tile;
-constexpr int kWMaxTI = 10;
-constexpr int kB = 4;  // tiles in flight per batch
+constexpr int kWMaxTI = 8;
 
 __host__ __device__ constexpr int ntiles(int TI) { return TI * (TI + 1) / 2; }
 __host__ __device__ constexpr int tidx(int I, int K) { return (I * (I + 1) >> 1) + K; }
 
+// Shared memory (doubles): the gathered points, a staging buffer for one generated
+// panel (generation is a compact runtime loop; the tiles then move to registers),
+// θ and the exp table.
 struct Layout {
-  int P, T, zb, lb, theta, etab, tab, total;
+  int P, G, theta, etab, total;
   __host__ __device__ constexpr Layout(int TI)
-      : P(0),
-        T(32 * TI),                  // packed lower tiles, tidx(I,K)
-        zb(T + 64 * ntiles(TI)),     // −L_JJ⁻¹, row-major
-        lb(zb + 64),                 // L_JJ, row-major
-        theta(lb + 64),
-        etab(theta + (int)(sizeof(Theta) / 8)),
-        tab(etab + 64),              // int16 (I | K << 8), tiles in column-major order
-        total(tab + (ntiles(TI) + 3) / 4) {}
+      : P(0), G(32 * TI), theta(G + 64 * TI), etab(theta + (int)(sizeof(Theta) / 8)), total(etab + 64) {}
   __host__ __device__ constexpr int bytes() const { return 8 * total; }
 };
+// Resident warps (= blocks) per SM the register budget targets (live tiles ≈ (TI/2)² + TI).
+__host__ __device__ constexpr int minb_for(int TI) { return TI >= 8 ? 14 : TI >= 6 ? 16 : 20; }
 
-__device__ __forceinline__ void dmma_if(double& d0, double& d1, double a, double b, int p) {
-  asm("{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n"
-      " @q mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n}\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b), "r"(p));
-}
-__device__ __forceinline__ double2 trsm_if(double2 c, double2 zn, double2 lj, int p) {
-  double x0 = 0.0, x1 = 0.0;
-  dmma_if(x0, x1, c.x, zn.x, p);
-  dmma_if(x0, x1, c.y, zn.y, p);
-  dmma_if(c.x, c.y, x0, lj.x, p);
-  dmma_if(c.x, c.y, x1, lj.y, p);
-  dmma_if(x0, x1, c.x, zn.x, p);
-  dmma_if(x0, x1, c.y, zn.y, p);
-  return make_double2(x0, x1);
+__device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+// Cholesky of one 8×8 tile spread over the warp (c0, c1 = this lane's C[g][2t], C[g][2t+1],
+// positive, lower part meaningful) → c0, c1 = L[g][2t], L[g][2t+1] (0 above the diagonal) and
+// z0, z1 = −(L⁻¹)[g][2t], −(L⁻¹)[g][2t+1].  Pivot j: the pivot is broadcast from lane
+// (j, j/2); every lane forms 1/L_jj by the same rsqrt steps as the other kernels; column j is
+// scaled with one residual correction per entry (each L_gj consistent with L_jj to an ulp);
+// the trailing entries get C[g][c] −= L_gj L_cj with L_gj, L_cj shuffled from column j's lanes.
+// The inverse is the same elimination applied to the identity.  Rows j ≥ N − 8J (the y row,
+// eliminated but never pivoted, and padding) only occur in the LAST tile, whose L and L⁻¹ no
+// solve reads; pivot checks (reading G15) and the d product over real rows j ≥ m run off the
+// chain; the y row's in-tile entries give u's last terms (qd, this lane's share).  jit: the
+// optional jitter mode's ε·σ² on the diagonal (reading G15b).
+__device__ __forceinline__ void factor_dist(double& c0, double& c1, double& z0, double& z1, int lane, int J, int m,
+                                            int N, double pfloor, double jit, double& prod, int& nbad, double& qd) {
+  const int g = lane >> 2, t = lane & 3, nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
+  if (g == 2 * t) c0 += jit;
+  if (g == 2 * t + 1) c1 += jit;
+  double rr[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int tj = j >> 1;
+    const double vj = (j & 1) ? c1 : c0;  // this lane's entry in column j (if t == tj)
+    const double p = shfl(vj, 4 * j + tj);
+    const double r = rsqrt_pos(p);
+    const double lv = p * r;
+    rr[j] = r;
+    {  // off the chain: pivot check and d (every lane holds the same p)
+      const bool real = j < nreal, ok = (p > pfloor) & (p <= 1.7976931348623157e308);
+      nbad += (real & !ok) ? 1 : 0;
+      prod *= (real & (j >= jm)) ? p : 1.0;
+    }
+    const double x = vj * r;
+    const double lval = (g > j) ? fma(fma(-x, lv, vj), r, x) : ((g == j) ? lv : 0.0);
+    if (t == tj) {
+      if (j & 1) c1 = lval;
+      else c0 = lval;
+    }
+    const double lgj = shfl(lval, 4 * g + tj);        // L[g][j]
+    const double lc0 = shfl(lval, 8 * t + tj);        // L[2t][j]
+    const double lc1 = shfl(lval, 8 * t + 4 + tj);    // L[2t+1][j]
+    if (g > j) {
+      if (2 * t > j) c0 = fma(-lgj, lc0, c0);
+      if (2 * t + 1 > j) c1 = fma(-lgj, lc1, c1);
+    }
+  }
+  if (2 * t > g) c0 = 0.0;  // upper part of L_JJ: zero (the panel solves read all 64 entries)
+  if (2 * t + 1 > g) c1 = 0.0;
+  if (g == yr) {            // the y row's entries in this tile: u's last terms (columns ≥ m)
+    if (2 * t < g && 2 * t >= jm) qd = fma(c0, c0, qd);
+    if (2 * t + 1 < g && 2 * t + 1 >= jm) qd = fma(c1, c1, qd);
+  }
+  // Z = L⁻¹ by the same elimination on the identity: row k scaled by 1/L_kk, then
+  // Z[g][·] −= L[g][k] Z[k][·] for g > k
+  z0 = (g == 2 * t) ? 1.0 : 0.0;
+  z1 = (g == 2 * t + 1) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (g == k) {
+      z0 *= rr[k];
+      z1 *= rr[k];
+    }
+    const double vk = (k & 1) ? c1 : c0;
+    const double lgk = shfl(vk, 4 * g + (k >> 1));  // L[g][k]
+    const double zk0 = shfl(z0, 4 * k + t), zk1 = shfl(z1, 4 * k + t);
+    if (g > k) {
+      z0 = fma(-lgk, zk0, z0);
+      z1 = fma(-lgk, zk1, z1);
+    }
+  }
+  z0 = neg(z0);
+  z1 = neg(z1);
 }
 
 template <int TI, int KIND>
-__global__ void __launch_bounds__(32) bv_block_w_kernel(
+__global__ void __launch_bounds__(32, minb_for(TI)) bv_block_w_kernel(
     const PointRec* __restrict__ pts, const int32_t* __restrict__ nbr, const BlockDesc* __restrict__ desc,
     const int32_t* __restrict__ list, const Theta* __restrict__ theta_dev, const double* __restrict__ exp_tab,
     double* __restrict__ out_u, double* __restrict__ out_d, unsigned long long* __restrict__ acc, int k_begin,
     const double* __restrict__ pre, const int64_t* __restrict__ pre_off, double jit) {
   constexpr Layout Ly(TI);
+  constexpr int NT = ntiles(TI);
   extern __shared__ __align__(16) double smem[];
   PointRec* P = reinterpret_cast<PointRec*>(smem + Ly.P);
-  double* T = smem + Ly.T;
-  double* zb = smem + Ly.zb;
-  double* lb = smem + Ly.lb;
+  double* G = smem + Ly.G;
   Theta* ths = reinterpret_cast<Theta*>(smem + Ly.theta);
   double* etab = smem + Ly.etab;
-  int16_t* tab = reinterpret_cast<int16_t*>(smem + Ly.tab);
 
   const int q = list[blockIdx.x];
   const BlockDesc ds = desc[q];
   const int m = ds.m, l = ds.l, N = m + l;
-  const int TJ = (N + 7) >> 3;  // column panels; TI = (N + 8) >> 3 (the bucket)
+  const int TJ = (N + 7) >> 3;  // column panels: TI or TI − 1 (TI = (N + 8) >> 3, the bucket)
   const int lane = threadIdx.x, g = lane >> 2, t = lane & 3;
   const double* preb = KIND == kPre ? pre + pre_off[q] : nullptr;
 
-  // a1/a2: θ, exp table, gathered points (neighbours first), tile list
+  // a1/a2: θ, exp table, gathered points (neighbours first); padding = far points
   etab[lane] = exp_tab[lane];
   etab[lane + 32] = exp_tab[lane + 32];
   if (lane < (int)(sizeof(Theta) / 8)) reinterpret_cast<double*>(ths)[lane] = reinterpret_cast<const double*>(theta_dev)[lane];
 #pragma unroll 1
   for (int i = lane; i < 8 * TI; i += 32) {
-    const double far = 1e30 * (double)(i + 1);  // padding: far points (exact zeros off the diagonal)
+    const double far = 1e30 * (double)(i + 1);
     PointRec r = {far, far, far, 0.0};
     if (i < N) r = pts[(i < m) ? nbr[ds.nbr_off + i] : ds.pstart + (i - m)];
     P[i] = r;
   }
-  int ntl = 0;  // tiles of the lower triangle, column-major (K < TJ): column K starts at colstart(K)
-  for (int K = 0; K < TJ; ++K)
-    for (int I = K; I < TI; ++I) {
-      if (ntl % 32 == lane) tab[ntl] = (int16_t)(I | (K << 8));
-      ++ntl;
-    }
   __syncwarp();
   const Theta& th = *ths;
 
-  // a3: every tile of the lower triangle, batches of kB in flight
-#pragma unroll 1
-  for (int e0 = 0; e0 < ntl; e0 += kB) {
-    double2 v[kB];
-#pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      const int e = e0 + u < ntl ? e0 + u : ntl - 1;
-      const int c = tab[e];
-      v[u] = gen_tile<KIND>(P, c & 0xff, c >> 8, g, t, N, th, etab, preb);
-    }
-#pragma unroll
-    for (int u = 0; u < kB; ++u) {
-      const int e = e0 + u < ntl ? e0 + u : ntl - 1;
-      const int c = tab[e];
-      sts2(T + 64 * tidx(c & 0xff, c >> 8) + 2 * lane, v[u].x, v[u].y);
-    }
-  }
-  __syncwarp();
-
   const int Iy = N >> 3, gy = N & 7;
   const double pfloor = kPivotFloor * th.sigma2;
-  double pm = 1.0, qd = 0.0, qd_in = 0.0;
-  int pe = 0, nbad = 0, cs = 0;  // cs = colstart(J)
+  double pm = 1.0, qd = 0.0;
+  int pe = 0, nbad = 0;
+  double2 T[NT];
+#pragma unroll
+  for (int K = 0; K < TI; ++K) {
+    if (K < TJ) {  // uniform (only the last panel can be absent)
+      // a3: panel K, tiles I = K..TI−1, four in flight, staged through shared memory
 #pragma unroll 1
-  for (int J = 0; J < TJ; ++J) {
-    factor_tile<true>(T + 64 * tidx(J, J), lb, zb, J, m, N, lane, pfloor, jit, pm, nbad, qd_in);  // a4/a7
-    int ex;
-    pm = frexp(pm, &ex);
-    pe += ex;
-    __syncwarp();
-    const double2 zn = lds2(zb + 2 * lane), lf = lds2(lb + 2 * lane);
-    // a5/a6: column J, I = J+1 .. TI−1
-#pragma unroll 1
-    for (int I0 = J + 1; I0 < TI; I0 += kB) {
-      double2 c[kB];
+      for (int i0 = K; i0 < TI; i0 += 4) {
+        double2 v[4];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) c[u] = lds2(T + 64 * tidx(I0 + u < TI ? I0 + u : TI - 1, J) + 2 * lane);
+        for (int u = 0; u < 4; ++u) v[u] = gen_tile<KIND>(P, i0 + u < TI ? i0 + u : TI - 1, K, g, t, N, th, etab, preb);
 #pragma unroll
-      for (int u = 0; u < kB; ++u) c[u] = trsm_if(c[u], zn, lf, I0 + u < TI);
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u < TI) sts2(G + 64 * (i0 + u) + 2 * lane, v[u].x, v[u].y);
+      }
+      __syncwarp();
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int I = I0 + u;
-        if (I < TI) {
-          sts2(T + 64 * tidx(I, J) + 2 * lane, c[u].x, c[u].y);
-          if (I == Iy && g == gy) qd += yrow_sq(c[u], J, t, m, N);
+      for (int I = K; I < TI; ++I) T[tidx(I, K)] = lds2(G + 64 * I + 2 * lane);
+      __syncwarp();
+      // a6: progressive subtraction of the earlier panels, K' ascending
+#pragma unroll
+      for (int Kp = 0; Kp < K; ++Kp)
+#pragma unroll
+        for (int I = K; I < TI; ++I) {
+          double2& c = T[tidx(I, K)];
+          dmma(c.x, c.y, T[tidx(I, Kp)].x, T[tidx(K, Kp)].x);
+          dmma(c.x, c.y, T[tidx(I, Kp)].y, T[tidx(K, Kp)].y);
         }
+      // a4/a7: the diagonal tile (positive C = −Ĉ)
+      double c0 = neg(T[tidx(K, K)].x), c1 = neg(T[tidx(K, K)].y), z0, z1;
+      factor_dist(c0, c1, z0, z1, lane, K, m, N, pfloor, jit, pm, nbad, qd);
+      int ex;
+      pm = frexp(pm, &ex);
+      pe += ex;
+      const double2 zn = make_double2(z0, z1), lf = make_double2(c0, c1);
+      // a5/a6: L(I,K) for I > K
+#pragma unroll
+      for (int I = K + 1; I < TI; ++I) {
+        T[tidx(I, K)] = trsm(T[tidx(I, K)], zn, lf);
+        if (I == Iy && g == gy) qd += yrow_sq(T[tidx(I, K)], K, t, m, N);
       }
     }
-    __syncwarp();
-    // a6: trailing tiles (I,K), J < K ≤ I, K < TJ — the suffix of the column-major list
-    cs += TI - J;
-#pragma unroll 1
-    for (int e0 = cs; e0 < ntl; e0 += kB) {
-      double2 c[kB], a[kB], b[kB];
-      int ti[kB];
-#pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int e = e0 + u < ntl ? e0 + u : ntl - 1;
-        const int cc = tab[e], I = cc & 0xff, K = cc >> 8;
-        ti[u] = tidx(I, K);
-        c[u] = lds2(T + 64 * ti[u] + 2 * lane);
-        a[u] = lds2(T + 64 * tidx(I, J) + 2 * lane);
-        b[u] = lds2(T + 64 * tidx(K, J) + 2 * lane);
-      }
-#pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int p = e0 + u < ntl;
-        dmma_if(c[u].x, c[u].y, a[u].x, b[u].x, p);
-        dmma_if(c[u].x, c[u].y, a[u].y, b[u].y, p);
-      }
-#pragma unroll
-      for (int u = 0; u < kB; ++u)
-        if (e0 + u < ntl) sts2(T + 64 * ti[u] + 2 * lane, c[u].x, c[u].y);
-    }
-    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) qd += __shfl_xor_sync(0xffffffffu, qd, o);
@@ -190,7 +215,7 @@ __global__ void __launch_bounds__(32) bv_block_w_kernel(
     int st = fail ? kNotPD : kOk;
     uint32_t cc[6] = {0, 0, 0, 0, 0, 0};
     const double logdet = fail ? failed_d() : log(pm) + (double)pe * 0.69314718055994530942;  // d = Σ_{j≥m} log p_j
-    const double quad = fail ? 0.0 : qd + qd_in;
+    const double quad = fail ? 0.0 : qd;
     if (!fail) {
       const double tk = -0.5 * (quad + logdet + (double)l * kLn2Pi);
       if (fixed_encode(tk, cc)) st = kTermRange;
@@ -214,11 +239,7 @@ static cudaError_t w_prep_ti() {
   const void* f[5] = {(const void*)wk::bv_block_w_kernel<TI, 0>, (const void*)wk::bv_block_w_kernel<TI, 1>,
                       (const void*)wk::bv_block_w_kernel<TI, 2>, (const void*)wk::bv_block_w_kernel<TI, 3>,
                       (const void*)wk::bv_block_w_kernel<TI, tile::kPre>};
-  for (int k = 0; k < 5 && e == cudaSuccess; ++k) {
-    e = cudaFuncSetAttribute(f[k], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(f[k], cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-  }
+  for (int k = 0; k < 5 && e == cudaSuccess; ++k) e = cudaFuncSetAttribute(f[k], cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   return e;
 }
 
@@ -245,7 +266,7 @@ static cudaError_t w_launch_ti(int kind, int nblocks, cudaStream_t s, const Poin
 cudaError_t prepare_block_w() {
   cudaError_t e = cudaSuccess;
 #define BV_P(T) if (e == cudaSuccess) e = w_prep_ti<T>();
-  BV_P(1) BV_P(2) BV_P(3) BV_P(4) BV_P(5) BV_P(6) BV_P(7) BV_P(8) BV_P(9) BV_P(10)
+  BV_P(1) BV_P(2) BV_P(3) BV_P(4) BV_P(5) BV_P(6) BV_P(7) BV_P(8)
 #undef BV_P
   return e;
 }
@@ -259,7 +280,7 @@ cudaError_t launch_block_w(int kind, int nblocks, int TI, cudaStream_t s, const 
 #define BV_T(T)                                                                                                  \
   case T:                                                                                                        \
     return w_launch_ti<T>(kind, nblocks, s, pts, nbr, desc, list, th, etab, u, d, acc, k_begin, pre, pre_off, jit);
-    BV_T(1) BV_T(2) BV_T(3) BV_T(4) BV_T(5) BV_T(6) BV_T(7) BV_T(8) BV_T(9) BV_T(10)
+    BV_T(1) BV_T(2) BV_T(3) BV_T(4) BV_T(5) BV_T(6) BV_T(7) BV_T(8)
 #undef BV_T
     default: return cudaErrorInvalidValue;
   }
