@@ -1,34 +1,36 @@
-// bv_block_v3.cu — the block kernel, warp-specialised pipeline.
+// bv_block_v3.cu — the large-block kernel (joint sizes N ≥ 64): one block per CTA,
+// warp-specialised.
 //
-// Same mathematics as bv_block_v2.cu (header there): the left-looking 8×8-tiled
-// Cholesky of the augmented joint matrix [[Σcon, Σcross, y_NN],[Σcrossᵀ, Σlk,
-// y_B]] of one block per CTA (Alg. 1 l.10-29), DMMA.8x8x4
-// panel updates, Matérn generated on the fly.  What changes is the schedule:
-// v2 ran every panel as three CTA-wide phases (diagonal factor ‖ update → row
-// solves → last update term), so each panel paid three full barriers and the
-// block's serial pivot chain waited for the bulk work every panel.  Here the
-// chain runs on its own warp and hands results to the three update warps
-// through named barriers (bar.arrive / bar.sync), one panel ahead:
+// One Cholesky of the augmented joint matrix [[Σcon, Σcross, y_NN],[Σcrossᵀ, Σlk,
+// y_B]] (Alg. 1 l.10-29, fused as in DESIGN.md §4), left-looking
+// over 8-wide column panels, FP64 MMA (DMMA.8x8x4) for every tile product, Matérn
+// generated on the fly.  A dedicated chain warp factors the diagonal tiles and
+// hands each panel to the three update warps through named barriers
+// (bar.arrive / bar.sync), one panel ahead:
 //
-//  diagonal warp D, iteration J:              update warps U (96 threads), iteration J:
-//    factor C(J,J)  → publish L_JJ, 1/L_jj      generate A(I,J+1), I ≥ J+2 (slots)
-//    sync  E  (U finished iteration J−1)         S(I) = Σ_{K<J} L(I,K) L(J+1,K)ᵀ (DMMA)
-//    arrive G                                    sync G
-//    P = A(J+1,J+1) − Σ_{K<J} L(J+1,K)L(J+1,K)ᵀ  L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2 (row solves)
-//    L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ (8 rows)         sync U-only barrier
-//    arrive F                                    sync F
-//    C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ         C(I,J+1) = A − S − L(I,J) L(J+1,J)ᵀ → slots
-//    → next J (no wait for the bulk)             arrive E
+//  chain warp, iteration J:                    update warps (96 threads), iteration J:
+//    factor C(J,J) across its lanes → publish    generate A(I,J+1) for their tiles I ≥ J+1
+//      L_JJ and L_JJ⁻¹ (tile::factor_dist)         straight into MMA accumulators, then
+//    sync  E  (updates of iteration J−1 done)      S ← S − L(I,K) L(J+1,K)ᵀ, K = 0..J−1
+//    arrive G                                      (progressive subtraction); warp 1 owns
+//    L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ                    the next diagonal tile → publishes it (P)
+//    sync H (P published) ; arrive F             sync G ; arrive H
+//    C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ         L(I,J) = C(I,J) L_JJ⁻ᵀ, I ≥ J+2
+//    → next J                                    sync F ; C(I,J+1) = S − L(I,J) L(J+1,J)ᵀ
+//                                                  → slots ; arrive E
 //
-// The diagonal tile never leaves the chain warp (it lives in a private 8×8
-// buffer); every other tile lives in one slot from generation through its
-// in-place solve to its last use (slot table: bv_host.cpp SlotTables, v3
-// schedule).  Non-PD blocks keep running the protocol on substituted pivots
-// (no early exit, so no warp can be left waiting at a barrier) and are flagged.
+// Panel solves are DMMA products with the explicit L_JJ⁻¹ plus one FP64
+// refinement step.  The diagonal tile lives in a private 8×8 buffer; every
+// other tile lives in one shared-memory slot from its store through its
+// in-place solve to its last use (slot table: bv_host.cpp SlotTables); joint
+// sizes past shared memory (N > 295) keep the slots in a global scratch.
+// Non-PD blocks keep running the protocol (NaN pivots, no early exit, so no
+// warp can be left waiting at a barrier) and are flagged.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "bv_common.cuh"
+#include "bv_tile.cuh"
 #include "matern.cuh"
 
 namespace bv {
@@ -111,78 +113,6 @@ __device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec
   if constexpr (KIND == kPre) v = pre_entry(pre, r, c, N, th.sigma2);
   else v = matern_kind<KIND>(sqdist(pr, pc), th, tab64);
   return (r == N) ? pc.v : v;  // the y row; padding entries are 0 by construction (far points)
-}
-
-// In-lane Cholesky of the 8×8 tile t (row-major lower, every lane holds it),
-// then L_JJ⁻¹ by columns (lane j solves L x = e_j).  Lanes 0..7 publish column
-// j of L_JJ⁻¹ (li), lane 0 all of L_JJ (lf), both in DMMA fragment order:
-// element (i,k) at 2(4i + (k&3)) + (k>>2).  The pivot chain carries no selects:
-// padding rows are far points (pivot σ², exactly zero coupling, so their rows
-// and columns of L_JJ and L_JJ⁻¹ are exactly decoupled and the padding columns
-// of every L(I,J) = C(I,J) L_JJ⁻ᵀ stay zero); the y row's "pivot" (eliminated,
-// never pivoted) only poisons rows below it in the LAST tile, which no solve
-// reads.  Pivot checks (reading G15) and the d product over real rows j ≥ m
-// run on the recorded pivots, off the chain.  jit: the optional jitter mode's
-// ε·σ² on the diagonal (reading G15b; harmless on padding and the y row).
-__device__ __forceinline__ void factor_tile(const double* t, double* lf, double* li, int J, int m, int N, int lane,
-                                            double pfloor, double jit, double& prod, int& nbad, double& qd) {
-  const int nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
-  double a[8][8], rr[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int k = 0; k <= i; ++k) a[i][k] = t[8 * i + k];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) a[i][i] += jit;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const double p = a[j][j];
-    const double r = rsqrt_pos(p);
-    const double lv = p * r;
-    {  // off the chain: pivot check (reading G15) and the d product over real rows ≥ m
-      const bool real = j < nreal, ok = (p > pfloor) & (p <= 1.7976931348623157e308);
-      nbad += (real & !ok) ? 1 : 0;
-      prod *= (real & (j >= jm)) ? p : 1.0;
-    }
-    rr[j] = r;
-    a[j][j] = lv;
-#pragma unroll
-    for (int i = j + 1; i < 8; ++i) {
-      const double x = a[i][j] * r;
-      a[i][j] = fma(fma(-x, lv, a[i][j]), r, x);
-    }
-#pragma unroll
-    for (int i = j + 1; i < 8; ++i)
-#pragma unroll
-      for (int k = j + 1; k <= i; ++k) a[i][k] = fma(-a[i][j], a[k][j], a[i][k]);
-  }
-#pragma unroll
-  for (int i = 1; i < 8; ++i)
-    if (i == yr) {
-#pragma unroll
-      for (int k = 0; k < i; ++k)
-        if (k >= jm) qd = fma(a[i][k], a[i][k], qd);
-    }
-  const int j = lane & 7;
-  // column j = lane & 7 of L⁻¹: x_i = (δ_ij − Σ_{k<i} L_ik x_k) / L_ii
-  double x[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    double s = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < i; ++k) s = fma(-a[i][k], x[k], s);
-    x[i] = s * rr[i];
-  }
-  if (lane < 8) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) li[2 * (4 * i + (j & 3)) + (j >> 2)] = x[i];
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) sts2(lf + 2 * (4 * i + k), k <= i ? a[i][k] : 0.0, k + 4 <= i ? a[i][k + 4] : 0.0);
-  }
 }
 
 // L(I,J) = C(I,J) L_JJ⁻ᵀ for one tile, in place (one warp): C is row-major,
@@ -312,7 +242,10 @@ __device__ __forceinline__ void u_column(double (&S)[MAXT][2], const double* slo
 // of TI ≤ 16 (MAXT ≤ 5, the bulk of c3/c4) and 4 of TI 17-18; 5 × 128 threads
 // caps registers at 102 (a few spills in the chain warp's in-lane factor,
 // measured +2.5 % at c4 over 4 CTAs with none).
-constexpr int v3_minb(int maxt) { return maxt >= 16 ? 2 : maxt <= 5 ? 5 : 4; }
+#ifndef BV_MINB5
+#define BV_MINB5 5
+#endif
+constexpr int v3_minb(int maxt) { return maxt >= 16 ? 2 : maxt <= 5 ? BV_MINB5 : 4; }
 // Joint sizes beyond what shared memory holds (TI > 37, N > 295: the paper's
 // conditioning sets reach 420-450) keep the same schedule
 // with the tile slots in a global-memory scratch (L1/L2-resident) instead of
@@ -362,7 +295,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   for (int i = tid; i < 8 * TI; i += kNT) {
     // padding rows/columns (i ≥ N, and the y row's own point): far-apart points, so every
     // padding entry off the diagonal is exactly 0 from Eq. (7) itself (x > 708 → 0) and no
-    // per-entry validity select is needed; padding pivots are substituted in factor_tile
+    // per-entry validity select is needed (padding pivots are σ², exactly decoupled)
     const double far = 1e30 * (double)(i + 1);
     PointRec r = {far, far, far, 0.0};
     if (i < N) r = pts[(i < m) ? nbr[ds.nbr_off + i] : ds.pstart + (i - m)];
@@ -394,13 +327,23 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
 
   if (uw == 0) {
     // ---------------------------------------------------------- chain warp
-    double pm = 1.0, qd_in = 0.0, qd_t = 0.0;
+    double pm = 1.0, qd_t = 0.0;
     int pe = 0, nbad = 0;
     for (int J = 0; J < TJ; ++J) {
       double* li = linv + 64 * (J & 1);
       double* lj = lfr + 64 * (J & 1);
       P3_T(t0);
-      factor_tile(dtile, lj, li, J, m, N, lane, pfloor, jit, pm, nbad, qd_in);  // a4/a7
+      {  // a4/a7: the diagonal tile factored across the warp's lanes (bv_tile.cuh factor_dist)
+        const double2 dv = lds2(dtile + 8 * g + 2 * t);
+        double c0 = dv.x, c1 = dv.y, z0, z1;
+        tile::factor_dist(c0, c1, z0, z1, lane, J, m, N, pfloor, jit, pm, nbad, qd_t);
+        // publish in this kernel's fragment order: element (i,k) at 2(4i + (k&3)) + (k>>2)
+        const int k0 = 2 * t, k1 = 2 * t + 1;
+        li[2 * (4 * g + (k0 & 3)) + (k0 >> 2)] = neg(z0);
+        li[2 * (4 * g + (k1 & 3)) + (k1 >> 2)] = neg(z1);
+        lj[2 * (4 * g + (k0 & 3)) + (k0 >> 2)] = c0;
+        lj[2 * (4 * g + (k1 & 3)) + (k1 >> 2)] = c1;
+      }
       int ex;
       pm = frexp(pm, &ex);
       pe += ex;
@@ -451,7 +394,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     // y-row contributions of the chain warp: in-lane part (identical in all lanes) + row solves
     for (int o = 16; o > 0; o >>= 1) qd_t += __shfl_xor_sync(0xffffffffu, qd_t, o);
     if (lane == 0) {
-      misc[1] = qd_in + qd_t;  // per-warp partials, summed in a fixed order below (bitwise reproducible)
+      misc[1] = qd_t;  // per-warp partials, summed in a fixed order below (bitwise reproducible)
       misc[4] = log(pm) + (double)pe * 0.69314718055994530942;  // d = Σ_{j≥m} log p_j
     }
   } else {

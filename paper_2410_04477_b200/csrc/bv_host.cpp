@@ -490,7 +490,7 @@ static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world
   const char* kenv = std::getenv("BV_KERNEL");
   const bool force_v3 = kenv && std::string(kenv) == "v3";
   const char* wenv = std::getenv("BV_WMAX");
-  const int wmax = force_v3 ? 0 : std::max(0, std::min(bv::w_max_ti(), wenv ? std::atoi(wenv) : 8));
+  const int wmax = force_v3 ? 0 : std::max(0, std::min(bv::w_max_ti(), wenv ? std::atoi(wenv) : 10));
   const int Nlimit = [&] {
     int N = 8;
     SlotTables st;

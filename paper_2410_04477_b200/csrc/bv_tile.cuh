@@ -155,5 +155,79 @@ __device__ __forceinline__ void factor_tile(const double* dg, double* lb, double
   }
 }
 
+__device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
+
+// Cholesky of one 8×8 tile spread over the warp (c0, c1 = this lane's C[g][2t], C[g][2t+1],
+// positive, lower part meaningful) → c0, c1 = L[g][2t], L[g][2t+1] (0 above the diagonal) and
+// z0, z1 = −(L⁻¹)[g][2t], −(L⁻¹)[g][2t+1].  Pivot j: the pivot is broadcast from lane
+// (j, j/2); every lane forms 1/L_jj by the same rsqrt steps as the other kernels; column j is
+// scaled with one residual correction per entry (each L_gj consistent with L_jj to an ulp);
+// the trailing entries get C[g][c] −= L_gj L_cj with L_gj, L_cj shuffled from column j's lanes.
+// The inverse is the same elimination applied to the identity.  Rows j ≥ N − 8J (the y row,
+// eliminated but never pivoted, and padding) only occur in the LAST tile, whose L and L⁻¹ no
+// solve reads; pivot checks (reading G15) and the d product over real rows j ≥ m run off the
+// chain; the y row's in-tile entries give u's last terms (qd, this lane's share).  jit: the
+// optional jitter mode's ε·σ² on the diagonal (reading G15b).
+__device__ __forceinline__ void factor_dist(double& c0, double& c1, double& z0, double& z1, int lane, int J, int m,
+                                            int N, double pfloor, double jit, double& prod, int& nbad, double& qd) {
+  const int g = lane >> 2, t = lane & 3, nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
+  if (g == 2 * t) c0 += jit;
+  if (g == 2 * t + 1) c1 += jit;
+  double rr[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int tj = j >> 1;
+    const double vj = (j & 1) ? c1 : c0;  // this lane's entry in column j (if t == tj)
+    const double p = shfl(vj, 4 * j + tj);
+    const double r = rsqrt_pos(p);
+    const double lv = p * r;
+    rr[j] = r;
+    {  // off the chain: pivot check and d (every lane holds the same p)
+      const bool real = j < nreal, ok = (p > pfloor) & (p <= 1.7976931348623157e308);
+      nbad += (real & !ok) ? 1 : 0;
+      prod *= (real & (j >= jm)) ? p : 1.0;
+    }
+    const double x = vj * r;
+    const double lval = (g > j) ? fma(fma(-x, lv, vj), r, x) : ((g == j) ? lv : 0.0);
+    if (t == tj) {
+      if (j & 1) c1 = lval;
+      else c0 = lval;
+    }
+    const double lgj = shfl(lval, 4 * g + tj);        // L[g][j]
+    const double lc0 = shfl(lval, 8 * t + tj);        // L[2t][j]
+    const double lc1 = shfl(lval, 8 * t + 4 + tj);    // L[2t+1][j]
+    if (g > j) {
+      if (2 * t > j) c0 = fma(-lgj, lc0, c0);
+      if (2 * t + 1 > j) c1 = fma(-lgj, lc1, c1);
+    }
+  }
+  if (2 * t > g) c0 = 0.0;  // upper part of L_JJ: zero (the panel solves read all 64 entries)
+  if (2 * t + 1 > g) c1 = 0.0;
+  if (g == yr) {            // the y row's entries in this tile: u's last terms (columns ≥ m)
+    if (2 * t < g && 2 * t >= jm) qd = fma(c0, c0, qd);
+    if (2 * t + 1 < g && 2 * t + 1 >= jm) qd = fma(c1, c1, qd);
+  }
+  // Z = L⁻¹ by the same elimination on the identity: row k scaled by 1/L_kk, then
+  // Z[g][·] −= L[g][k] Z[k][·] for g > k
+  z0 = (g == 2 * t) ? 1.0 : 0.0;
+  z1 = (g == 2 * t + 1) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    if (g == k) {
+      z0 *= rr[k];
+      z1 *= rr[k];
+    }
+    const double vk = (k & 1) ? c1 : c0;
+    const double lgk = shfl(vk, 4 * g + (k >> 1));  // L[g][k]
+    const double zk0 = shfl(z0, 4 * k + t), zk1 = shfl(z1, 4 * k + t);
+    if (g > k) {
+      z0 = fma(-lgk, zk0, z0);
+      z1 = fma(-lgk, zk1, z1);
+    }
+  }
+  z0 = neg(z0);
+  z1 = neg(z1);
+}
+
 }  // namespace tile
 }  // namespace bv
