@@ -329,27 +329,33 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     // ---------------------------------------------------------- chain warp
     double pm = 1.0, qd_t = 0.0;
     int pe = 0, nbad = 0;
+    // the chain's tiles stay in registers in the MMA accumulator layout (lane (g,t): row g,
+    // columns 2t, 2t+1); products use the k-permuted form of bv_tile.cuh
+    double c0, c1;
+    {
+      const double2 dv = lds2(dtile + 8 * g + 2 * t);  // C(0,0)
+      c0 = dv.x;
+      c1 = dv.y;
+    }
     for (int J = 0; J < TJ; ++J) {
       double* li = linv + 64 * (J & 1);
       double* lj = lfr + 64 * (J & 1);
       P3_T(t0);
-      {  // a4/a7: the diagonal tile factored across the warp's lanes (bv_tile.cuh factor_dist)
-        const double2 dv = lds2(dtile + 8 * g + 2 * t);
-        double c0 = dv.x, c1 = dv.y, z0, z1;
-        tile::factor_dist(c0, c1, z0, z1, lane, J, m, N, pfloor, jit, pm, nbad, qd_t);
-        // publish in this kernel's fragment order: element (i,k) at 2(4i + (k&3)) + (k>>2)
+      // a4/a7: the diagonal tile factored across the warp's lanes (bv_tile.cuh factor_dist)
+      double z0, z1;
+      tile::factor_dist(c0, c1, z0, z1, lane, J, m, N, pfloor, jit, pm, nbad, qd_t);
+      {  // publish L_JJ, L_JJ⁻¹ for the update warps in this kernel's fragment order:
+         // element (i,k) at 2(4i + (k&3)) + (k>>2)
         const int k0 = 2 * t, k1 = 2 * t + 1;
         li[2 * (4 * g + (k0 & 3)) + (k0 >> 2)] = neg(z0);
         li[2 * (4 * g + (k1 & 3)) + (k1 >> 2)] = neg(z1);
         lj[2 * (4 * g + (k0 & 3)) + (k0 >> 2)] = c0;
         lj[2 * (4 * g + (k1 & 3)) + (k1 >> 2)] = c1;
       }
+      const double2 zn = make_double2(z0, z1), lf = make_double2(c0, c1);
       int ex;
       pm = frexp(pm, &ex);
       pe += ex;
-      __syncwarp();
-      const double2 bi = lds2(li + 2 * lane);  // this lane's fragments of L_JJ⁻¹ and L_JJ
-      const double2 bl = lds2(lj + 2 * lane);
       P3_ADD(0, t0);
       P3_T(t1);
       // U finished iteration J−1 (so it has consumed G, F, H of J−1: a named
@@ -363,31 +369,31 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         // TJ, below the last diagonal tile — its solve is this warp's (U only
         // handles tiles I ≥ J+2)
         if (TI > TJ) {
-          const double2 d = tile_trsm(slot_at(slots, tabu[TJ * TI + J]), bi, bl, g, t);
+          const double2 cv = lds2(slot_at(slots, tabu[TJ * TI + J]) + 8 * g + 2 * t);
+          const double2 d = tile::trsm(make_double2(neg(cv.x), neg(cv.y)), zn, lf);
           if (g == (N & 7)) qd_t += yrow_sq(d, J, t, m, N);
         }
         break;
       }
       P3_T(t3);
-      // L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ (a5/a6)
+      // L(J+1,J) = C(J+1,J) L_JJ⁻ᵀ (a5/a6), in registers (explicit inverse + one refinement)
       double* tj = slot_at(slots, tabu[(J + 1) * TI + J]);
-      {
-        const double2 d = tile_trsm(tj, bi, bl, g, t);
-        if (8 * (J + 1) + g == N) qd_t += yrow_sq(d, J, t, m, N);  // the y row: u += Σ_{j≥m} z_j²
-      }
-      __syncwarp();
-      const double2 lf = lds2(tj + 2 * lane);  // read before F: slot may be recycled
+      const double2 cv = lds2(tj + 8 * g + 2 * t);
+      const double2 x = tile::trsm(make_double2(neg(cv.x), neg(cv.y)), zn, lf);
+      if (8 * (J + 1) + g == N) qd_t += yrow_sq(x, J, t, m, N);  // the y row: u += Σ_{j≥m} z_j²
+      // → the slot in fragment order (the update warps' b operand of their final term)
+      tj[8 * g + 2 * ((2 * t) & 3) + (t >> 1)] = x.x;
+      tj[8 * g + 2 * ((2 * t + 1) & 3) + (t >> 1)] = x.y;
       P3_ADD(3, t3);
       P3_T(t4);
       bar_sync(kBarH, kNT);  // the update warps published P(J+1,J+1)
       const double2 pp = lds2(ptile + 8 * g + 2 * t);  // read before F: U regenerates ptile after F
       bar_arrive(kBarF, kNT);
-      // C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ → dtile
-      double p0 = pp.x, p1 = pp.y;
-      dmma884(p0, p1, neg(lf.x), lf.x);
-      dmma884(p0, p1, neg(lf.y), lf.y);
-      sts2(dtile + 8 * g + 2 * t, p0, p1);
-      __syncwarp();
+      // C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ, straight into the next factorisation
+      c0 = pp.x;
+      c1 = pp.y;
+      dmma884(c0, c1, neg(x.x), x.x);
+      dmma884(c0, c1, neg(x.y), x.y);
       P3_ADD(4, t4);
     }
     if (nbad && lane == 0) misc[2] = 1.0;
