@@ -114,7 +114,6 @@ __device__ __forceinline__ void factor_tile(const double* dg, double* lb, double
       nbad += (real & !ok) ? 1 : 0;
       prod *= (real & (j >= jm)) ? p : 1.0;
     }
-    rr[j] = r;
     a[j][j] = lv;
 #pragma unroll
     for (int i = j + 1; i < 8; ++i) {
@@ -163,7 +162,7 @@ __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0
 // (j, j/2); every lane forms 1/L_jj by the same rsqrt steps as the other kernels; column j is
 // scaled with one residual correction per entry (each L_gj consistent with L_jj to an ulp);
 // the trailing entries get C[g][c] −= L_gj L_cj with L_gj, L_cj shuffled from column j's lanes.
-// The inverse is the same elimination applied to the identity.  Rows j ≥ N − 8J (the y row,
+// The inverse is the same elimination applied to the identity, one step behind.  Rows j ≥ N − 8J (the y row,
 // eliminated but never pivoted, and padding) only occur in the LAST tile, whose L and L⁻¹ no
 // solve reads; pivot checks (reading G15) and the d product over real rows j ≥ m run off the
 // chain; the y row's in-tile entries give u's last terms (qd, this lane's share).  jit: the
@@ -173,7 +172,11 @@ __device__ __forceinline__ void factor_dist(double& c0, double& c1, double& z0, 
   const int g = lane >> 2, t = lane & 3, nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
   if (g == 2 * t) c0 += jit;
   if (g == 2 * t + 1) c1 += jit;
-  double rr[8];
+  // Z = L⁻¹ by the same elimination on the identity, one step behind the factorisation
+  // (step j needs column j of L and rows < j of Z): row j scaled by 1/L_jj, then
+  // Z[g][·] −= L[g][j] Z[j][·] for g > j — the two dependency chains overlap
+  z0 = (g == 2 * t) ? 1.0 : 0.0;
+  z1 = (g == 2 * t + 1) ? 1.0 : 0.0;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const int tj = j >> 1;
@@ -181,7 +184,6 @@ __device__ __forceinline__ void factor_dist(double& c0, double& c1, double& z0, 
     const double p = shfl(vj, 4 * j + tj);
     const double r = rsqrt_pos(p);
     const double lv = p * r;
-    rr[j] = r;
     {  // off the chain: pivot check and d (every lane holds the same p)
       const bool real = j < nreal, ok = (p > pfloor) & (p <= 1.7976931348623157e308);
       nbad += (real & !ok) ? 1 : 0;
@@ -200,30 +202,21 @@ __device__ __forceinline__ void factor_dist(double& c0, double& c1, double& z0, 
       if (2 * t > j) c0 = fma(-lgj, lc0, c0);
       if (2 * t + 1 > j) c1 = fma(-lgj, lc1, c1);
     }
+    if (g == j) {
+      z0 *= r;
+      z1 *= r;
+    }
+    const double zj0 = shfl(z0, 4 * j + t), zj1 = shfl(z1, 4 * j + t);
+    if (g > j) {
+      z0 = fma(-lgj, zj0, z0);
+      z1 = fma(-lgj, zj1, z1);
+    }
   }
   if (2 * t > g) c0 = 0.0;  // upper part of L_JJ: zero (the panel solves read all 64 entries)
   if (2 * t + 1 > g) c1 = 0.0;
   if (g == yr) {            // the y row's entries in this tile: u's last terms (columns ≥ m)
     if (2 * t < g && 2 * t >= jm) qd = fma(c0, c0, qd);
     if (2 * t + 1 < g && 2 * t + 1 >= jm) qd = fma(c1, c1, qd);
-  }
-  // Z = L⁻¹ by the same elimination on the identity: row k scaled by 1/L_kk, then
-  // Z[g][·] −= L[g][k] Z[k][·] for g > k
-  z0 = (g == 2 * t) ? 1.0 : 0.0;
-  z1 = (g == 2 * t + 1) ? 1.0 : 0.0;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    if (g == k) {
-      z0 *= rr[k];
-      z1 *= rr[k];
-    }
-    const double vk = (k & 1) ? c1 : c0;
-    const double lgk = shfl(vk, 4 * g + (k >> 1));  // L[g][k]
-    const double zk0 = shfl(z0, 4 * k + t), zk1 = shfl(z1, 4 * k + t);
-    if (g > k) {
-      z0 = fma(-lgk, zk0, z0);
-      z1 = fma(-lgk, zk1, z1);
-    }
   }
   z0 = neg(z0);
   z1 = neg(z1);

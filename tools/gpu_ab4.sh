@@ -8,3 +8,6 @@ for lib in $D/libbv.so $D/libbv_prev.so; do
   BV_LIB_PATH=$lib timeout 300 python bench.py --config c4 --no-cpu-baseline --no-ablation --steps 100 > $O/c4_${n}_$r.log 2>&1
 done; done
 echo done > $O/done
+for lib in $D/libbv.so $D/libbv_prev.so; do n=$(basename $lib .so)
+  BV_LIB_PATH=$lib timeout 300 python bench.py --config c5 --m 30 --no-cpu-baseline --no-ablation --steps 50 > $O/c5m30_${n}.log 2>&1
+done
