@@ -188,55 +188,80 @@ __device__ __forceinline__ double* slot_at(double* base, unsigned slot) {
   return reinterpret_cast<double*>(reinterpret_cast<char*>(base) + (slot << 9));
 }
 
-// Update-warp column work for NS tiles I = J+uw+3s of column J+1 (warp 1's first
-// tile is the next diagonal tile): generate A(I,J+1) (Eq. 7) straight into the
-// MMA accumulators (lane (g,t): row g, columns 2t, 2t+1), then subtract the
-// updates of panels K < J progressively, S ← S − L(I,K) L(J+1,K)ᵀ in increasing
-// K — the rounding order of a right-looking elimination (each update rounds
-// against the partially reduced value, not against the full sum of updates),
-// which on ill-conditioned blocks is several times more accurate than summing
-// the updates and subtracting once.
-template <int NS, int MAXT, int KIND>
-__device__ __forceinline__ void u_column(double (&S)[MAXT][2], const double* slots, const int16_t* tab, int TI, int J,
-                                         int uw, int lane, const PointRec* P, int N, const Theta& th,
+// Update-warp column work for this warp's ns tiles I = J+uw+3s of column J+1 (warp 1's
+// first tile is the next diagonal tile): generate A(I,J+1) (Eq. 7) straight into the MMA
+// accumulators (lane (g,t): row g, columns 2t, 2t+1), then subtract the updates of panels
+// K < J progressively, S ← S − L(I,K) L(J+1,K)ᵀ in increasing K — the rounding order of a
+// right-looking elimination (each update rounds against the partially reduced value, not
+// against the full sum of updates), which on ill-conditioned blocks is several times more
+// accurate than summing the updates and subtracting once.
+// The tiles go two at a time through ONE copy of the generation and of the K loop (plus a
+// single-tile K loop for an odd tail), the results placed into S by compile-time selects:
+// one code path for every tile count keeps the kernel's hot code small (per-tile-count
+// instantiations put the co-resident warps on different code copies: instruction-fetch
+// stalls, ncu stall_no_inst).
+template <int MAXT>
+__device__ __forceinline__ void u_place(double (&S)[MAXT][2], int s, double v0, double v1) {
+#pragma unroll
+  for (int q = 0; q < MAXT; ++q)
+    if (q == s) {
+      S[q][0] = v0;
+      S[q][1] = v1;
+    }
+}
+template <int MAXT, int KIND>
+__device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const double* slots, const int16_t* tab, int TI,
+                                         int J, int uw, int lane, const PointRec* P, int N, const Theta& th,
                                          const double* etab, const double* pre) {
   const int g = lane >> 2, t = lane & 3, c0 = 8 * (J + 1) + 2 * t;
   const PointRec pc0 = P[c0], pc1 = P[c0 + 1];
-  // one tile at a time (a runtime loop, the result placed by a compile-time select): the
-  // Matérn temporaries of one tile in flight, not of all NS, keep the 102-register budget
-#pragma unroll 1
-  for (int s = 0; s < NS; ++s) {
-    const int r = 8 * (J + uw + (kW - 1) * s) + g;
-    const PointRec pr = P[r];
-    const double v0 = joint_entry<KIND>(pr, pc0, r, c0, N, th, etab, pre);
-    const double v1 = joint_entry<KIND>(pr, pc1, r, c0 + 1, N, th, etab, pre);
-#pragma unroll
-    for (int q = 0; q < NS; ++q)
-      if (q == s) {
-        S[q][0] = v0;
-        S[q][1] = v1;
-      }
-  }
-  // slot s of this lane's fragment pair: one shift-add from an unsigned 16-bit slot index
   const double* sl = slots + 2 * lane;
   const uint16_t* tJ = reinterpret_cast<const uint16_t*>(tab) + (J + 1) * TI;
-  const uint16_t* tI[NS];
-#pragma unroll
-  for (int s = 0; s < NS; ++s) tI[s] = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (kW - 1) * s) * TI;
-#pragma unroll 2
-  for (int K = 0; K < J; ++K) {
-    const double2 b = lds2(slot_at(sl, tJ[K]));
-    const double bx = neg(b.x), by = neg(b.y);
-#pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      const double2 a = lds2(slot_at(sl, tI[s][K]));
-      dmma884(S[s][0], S[s][1], a.x, bx);
-      dmma884(S[s][0], S[s][1], a.y, by);
+#pragma unroll 1
+  for (int s = 0; s < ns; s += 2) {
+    const bool two = s + 1 < ns;  // warp-uniform
+    double a[2][2];
+#pragma unroll 1
+    for (int u = 0; u < (two ? 2 : 1); ++u) {
+      const int r = 8 * (J + uw + (kW - 1) * (s + u)) + g;
+      const PointRec pr = P[r];
+      const double v0 = joint_entry<KIND>(pr, pc0, r, c0, N, th, etab, pre);
+      const double v1 = joint_entry<KIND>(pr, pc1, r, c0 + 1, N, th, etab, pre);
+      if (u == 0) {
+        a[0][0] = v0;
+        a[0][1] = v1;
+      } else {
+        a[1][0] = v0;
+        a[1][1] = v1;
+      }
     }
+    const uint16_t* t0 = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (kW - 1) * s) * TI;
+    if (two) {
+      const uint16_t* t1 = t0 + (kW - 1) * TI;
+#pragma unroll 2
+      for (int K = 0; K < J; ++K) {
+        const double2 b = lds2(slot_at(sl, tJ[K]));
+        const double bx = neg(b.x), by = neg(b.y);
+        const double2 x0 = lds2(slot_at(sl, t0[K]));
+        const double2 x1 = lds2(slot_at(sl, t1[K]));
+        dmma884(a[0][0], a[0][1], x0.x, bx);
+        dmma884(a[1][0], a[1][1], x1.x, bx);
+        dmma884(a[0][0], a[0][1], x0.y, by);
+        dmma884(a[1][0], a[1][1], x1.y, by);
+      }
+      u_place(S, s + 1, a[1][0], a[1][1]);
+    } else {
+#pragma unroll 2
+      for (int K = 0; K < J; ++K) {
+        const double2 b = lds2(slot_at(sl, tJ[K]));
+        const double2 x0 = lds2(slot_at(sl, t0[K]));
+        dmma884(a[0][0], a[0][1], x0.x, neg(b.x));
+        dmma884(a[0][0], a[0][1], x0.y, neg(b.y));
+      }
+    }
+    u_place(S, s, a[0][0], a[0][1]);
   }
 }
-
-
 
 // CTAs per SM the register allocation targets: shared memory admits 5 blocks
 // of TI ≤ 16 (MAXT ≤ 5, the bulk of c3/c4) and 4 of TI 17-18; 5 × 128 threads
@@ -416,16 +441,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         // a3 + a6: this warp's tiles of column J+1, generated into registers and reduced by
         // the panels K < J (exact tile count per warp: no predicated-off work)
         const int ns = (TI - J - 1 - (uw - 1) + (kW - 2)) / (kW - 1);
-        switch (ns) {
-#define BV_NS(n)                                                                                              \
-  case n:                                                                                                     \
-    if (MAXT >= n) u_column<(MAXT >= n ? n : 1), MAXT, KIND>(S, slots, tab, TI, J, uw, lane, P, N, th, etab, preb); \
-    break;
-          BV_NS(1) BV_NS(2) BV_NS(3) BV_NS(4) BV_NS(5) BV_NS(6) BV_NS(7) BV_NS(8) BV_NS(9) BV_NS(10) BV_NS(11)
-          BV_NS(12) BV_NS(13) BV_NS(14) BV_NS(15) BV_NS(16) BV_NS(17) BV_NS(18) BV_NS(19) BV_NS(20)
-#undef BV_NS
-          default: break;
-        }
+        u_column<MAXT, KIND>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb);
         // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp (warp 1 owns the tile)
         if (uw == 1) sts2(ptile + 8 * g + 2 * t, S[0][0], S[0][1]);
         P3_ADD(6, u6);
