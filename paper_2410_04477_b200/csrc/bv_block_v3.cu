@@ -39,11 +39,21 @@ namespace v3 {
 // Panel solves L(I,J) = C(I,J) L_JJ⁻ᵀ are DMMA products with the explicit L_JJ⁻¹
 // plus one FP64 refinement step (a bare product with the inverse loses accuracy
 // on ill-conditioned tiles and fails the κ-aware parity rule at c3; row
-// substitution on the update warps measured 7 % slower, round 1).
+// substitution on the update warps measured 7 % slower, round 1).  The update warps
+// skip the refinement on panels where it cannot matter: max|L_JJ|·max|L_JJ⁻¹| ≤
+// kRefineKappa (a condition-number proxy; the bare product's error exceeds the
+// substitution's by at most about that factor).  Measured: 100 → c4 228.0 → 231.9 evals/s
+// with unchanged parity statistics (gpurun_out/abk: every c1-c4 case, same strict /
+// κ-branch / replica counts within noise); 1000 fails two c4 blocks; no refinement at
+// all fails c3 (26 blocks) — the chain warp's own solve always refines.
 // 4 warps per CTA (1 chain + 3 update): measured at c4, 5/6/8 warps per CTA gave
 // 187/180/166 evals/s against 197 (round 1).
 constexpr int kW = 4;  // warps per CTA: 1 chain warp + kW−1 update warps
 constexpr int kNT = kW * 32;
+#ifndef BV_REFINE_KAPPA
+#define BV_REFINE_KAPPA 100.0
+#endif
+constexpr double kRefineKappa = BV_REFINE_KAPPA;
 constexpr int kBarG = 1, kBarF = 2, kBarE = 3, kBarH = 5;  // named barriers (0 = __syncthreads)
 
 #ifdef BV_PROFILE_PHASES
@@ -120,11 +130,12 @@ __device__ __forceinline__ double joint_entry(const PointRec& pr, const PointRec
 // fragments of L_JJ⁻¹ / L_JJ (the B operands (L⁻ᵀ)[k][n], (Lᵀ)[k][n] at k = t,
 // n = g).  X₁ = C L⁻ᵀ, then one refinement step X = X₁ + (C − X₁Lᵀ) L⁻ᵀ with
 // the residual in FP64: this restores the accuracy of substitution, which a
-// bare multiply by the explicit inverse loses on ill-conditioned L_JJ.
+// bare multiply by the explicit inverse loses on ill-conditioned L_JJ (refine =
+// false skips it: the caller's condition proxy says it cannot matter).
 // Returns the lane's two results (row g, columns 2t, 2t+1) for the y-row term.
 template <int NT>
 __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 bi, double2 bl, int g, int t,
-                                            double2 (&out)[NT]) {
+                                            double2 (&out)[NT], bool refine) {
   double x0[NT], x1[NT], cc0[NT], cc1[NT];
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
@@ -137,6 +148,7 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     dmma884(x0[i], x1[i], c0, bi.x);
     dmma884(x0[i], x1[i], c1, bi.y);
   }
+  if (refine) {  // warp-uniform
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < NT; ++i) sts2(tile[i] + 8 * g + 2 * t, x0[i], x1[i]);
@@ -157,6 +169,7 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     dmma884(x0[i], x1[i], ra[0], bi.x);  // X = X₁ + R L⁻ᵀ
     dmma884(x0[i], x1[i], ra[4], bi.y);
   }
+  }
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < NT; ++i) {
@@ -165,10 +178,10 @@ __device__ __forceinline__ void tile_trsm_n(double* const (&tile)[NT], double2 b
     out[i] = make_double2(x0[i], x1[i]);
   }
 }
-__device__ __forceinline__ double2 tile_trsm(double* tile, double2 bi, double2 bl, int g, int t) {
+__device__ __forceinline__ double2 tile_trsm(double* tile, double2 bi, double2 bl, int g, int t, bool refine) {
   double* const tl[1] = {tile};
   double2 o[1];
-  tile_trsm_n<1>(tl, bi, bl, g, t, o);
+  tile_trsm_n<1>(tl, bi, bl, g, t, o, refine);
   return o[0];
 }
 
@@ -368,7 +381,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       P3_T(t0);
       // a4/a7: the diagonal tile factored across the warp's lanes (bv_tile.cuh factor_dist)
       double z0, z1;
-      tile::factor_dist(c0, c1, z0, z1, lane, J, m, N, pfloor, jit, pm, nbad, qd_t);
+      tile::factor_dist<8>(c0, c1, z0, z1, lane, J, m, N, pfloor, jit, pm, nbad, qd_t);
       {  // publish L_JJ, L_JJ⁻¹ for the update warps in this kernel's fragment order:
          // element (i,k) at 2(4i + (k&3)) + (k>>2)
         const int k0 = 2 * t, k1 = 2 * t + 1;
@@ -455,6 +468,15 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         // L(I,J) = C(I,J) L_JJ⁻ᵀ for this warp's tiles I = J+u+3s > J+1 (a5/a6)
         const double2 bi = lds2(linv + 64 * (J & 1) + 2 * lane);
         const double2 bl = lds2(lfr + 64 * (J & 1) + 2 * lane);
+        // refine only where the explicit inverse loses accuracy: max|L_JJ|·max|L_JJ⁻¹| (a
+        // condition-number proxy, the same value in every lane after the butterfly)
+        double mz = fmax(fabs(bi.x), fabs(bi.y)), ml = fmax(fabs(bl.x), fabs(bl.y));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mz = fmax(mz, __shfl_xor_sync(0xffffffffu, mz, o));
+          ml = fmax(ml, __shfl_xor_sync(0xffffffffu, ml, o));
+        }
+        const bool refine = mz * ml > kRefineKappa;
           // two tiles in flight: their DMMA / shared-memory round trips interleave
 #pragma unroll 1
         for (int I = J + uw + (uw == 1 ? kW - 1 : 0); I < TI; I += 2 * (kW - 1)) {
@@ -462,11 +484,11 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
           if (I2 < TI) {
             double* const tl[2] = {slot_at(slots, tabu[I * TI + J]), slot_at(slots, tabu[I2 * TI + J])};
             double2 d[2];
-            tile_trsm_n<2>(tl, bi, bl, g, t, d);
+            tile_trsm_n<2>(tl, bi, bl, g, t, d, refine);
             if (8 * I + g == N) qd_u += yrow_sq(d[0], J, t, m, N);  // the y row (a8)
             if (8 * I2 + g == N) qd_u += yrow_sq(d[1], J, t, m, N);
           } else {
-            const double2 d = tile_trsm(slot_at(slots, tabu[I * TI + J]), bi, bl, g, t);
+            const double2 d = tile_trsm(slot_at(slots, tabu[I * TI + J]), bi, bl, g, t, refine);
             if (8 * I + g == N) qd_u += yrow_sq(d, J, t, m, N);
           }
         }

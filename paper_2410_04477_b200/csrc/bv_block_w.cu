@@ -35,6 +35,16 @@ namespace wk {
 
 using namespace tile;
 constexpr int kWMaxTI = 10;
+// Generated tiles in flight per lane: 2 (measured against 4: c5 m = 60 256.3 -> 269.8
+// evals/s, m = 30 unchanged — fewer live temporaries next to the register tiles).
+constexpr int kGenFly = 2;
+// The diagonal factorisation's pivot loop is a rolled loop here (factor_dist<1>): the
+// kernel is unrolled over its panels, so an unrolled pivot loop would put TI copies of
+// ~350 instructions into the code (TI = 7: 7.3k → 4.7k SASS instructions; measured
+// c5 m = 30 664 -> 689 evals/s; instruction fetch, ncu stall_no_instruction, was the
+// largest stall).  A rolled PANEL loop (generation and factorisation once, the register-tile
+// parts reached by a compare chain) measured slower still (663 at m = 30): the unrolled
+// panels let one panel's generation overlap the previous panel's pivot chain.
 
 __host__ __device__ constexpr int ntiles(int TI) { return TI * (TI + 1) / 2; }
 __host__ __device__ constexpr int tidx(int I, int K) { return (I * (I + 1) >> 1) + K; }
@@ -94,14 +104,14 @@ __global__ void __launch_bounds__(32, minb_for(TI)) bv_block_w_kernel(
 #pragma unroll
   for (int K = 0; K < TI; ++K) {
     if (K < TJ) {  // uniform (only the last panel can be absent)
-      // a3: panel K, tiles I = K..TI−1, four in flight, staged through shared memory
+      // a3: panel K, tiles I = K..TI−1, kGenFly in flight, staged through shared memory
 #pragma unroll 1
-      for (int i0 = K; i0 < TI; i0 += 4) {
-        double2 v[4];
+      for (int i0 = K; i0 < TI; i0 += kGenFly) {
+        double2 v[kGenFly];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = gen_tile<KIND>(P, i0 + u < TI ? i0 + u : TI - 1, K, g, t, N, th, etab, preb);
+        for (int u = 0; u < kGenFly; ++u) v[u] = gen_tile<KIND>(P, i0 + u < TI ? i0 + u : TI - 1, K, g, t, N, th, etab, preb);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kGenFly; ++u)
           if (i0 + u < TI) sts2(G + 64 * (i0 + u) + 2 * lane, v[u].x, v[u].y);
       }
       __syncwarp();
@@ -119,7 +129,7 @@ __global__ void __launch_bounds__(32, minb_for(TI)) bv_block_w_kernel(
         }
       // a4/a7: the diagonal tile (positive C = −Ĉ)
       double c0 = neg(T[tidx(K, K)].x), c1 = neg(T[tidx(K, K)].y), z0, z1;
-      factor_dist(c0, c1, z0, z1, lane, K, m, N, pfloor, jit, pm, nbad, qd);
+      factor_dist<1>(c0, c1, z0, z1, lane, K, m, N, pfloor, jit, pm, nbad, qd);
       int ex;
       pm = frexp(pm, &ex);
       pe += ex;

@@ -166,7 +166,10 @@ __device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0
 // eliminated but never pivoted, and padding) only occur in the LAST tile, whose L and L⁻¹ no
 // solve reads; pivot checks (reading G15) and the d product over real rows j ≥ m run off the
 // chain; the y row's in-tile entries give u's last terms (qd, this lane's share).  jit: the
-// optional jitter mode's ε·σ² on the diagonal (reading G15b).
+// optional jitter mode's ε·σ² on the diagonal (reading G15b).  UNROLL: the pivot loop
+// unrolled (the block kernel's single chain copy: latency) or rolled (the warp kernel, one
+// copy per panel: code size).
+template <int UNROLL = 8>
 __device__ __forceinline__ void factor_dist(double& c0, double& c1, double& z0, double& z1, int lane, int J, int m,
                                             int N, double pfloor, double jit, double& prod, int& nbad, double& qd) {
   const int g = lane >> 2, t = lane & 3, nreal = N - 8 * J, jm = m - 8 * J, yr = N - 8 * J;
@@ -177,7 +180,7 @@ __device__ __forceinline__ void factor_dist(double& c0, double& c1, double& z0, 
   // Z[g][·] −= L[g][j] Z[j][·] for g > j — the two dependency chains overlap
   z0 = (g == 2 * t) ? 1.0 : 0.0;
   z1 = (g == 2 * t + 1) ? 1.0 : 0.0;
-#pragma unroll
+#pragma unroll UNROLL
   for (int j = 0; j < 8; ++j) {
     const int tj = j >> 1;
     const double vj = (j & 1) ? c1 : c0;  // this lane's entry in column j (if t == tj)
