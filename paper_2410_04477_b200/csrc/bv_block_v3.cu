@@ -234,19 +234,14 @@ __device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const dou
   for (int s = 0; s < ns; s += 2) {
     const bool two = s + 1 < ns;  // warp-uniform
     double a[2][2];
-#pragma unroll 1
-    for (int u = 0; u < (two ? 2 : 1); ++u) {
-      const int r = 8 * (J + uw + (kW - 1) * (s + u)) + g;
-      const PointRec pr = P[r];
-      const double v0 = joint_entry<KIND>(pr, pc0, r, c0, N, th, etab, pre);
-      const double v1 = joint_entry<KIND>(pr, pc1, r, c0 + 1, N, th, etab, pre);
-      if (u == 0) {
-        a[0][0] = v0;
-        a[0][1] = v1;
-      } else {
-        a[1][0] = v0;
-        a[1][1] = v1;
-      }
+    {  // both tiles' entries in flight (an odd tail recomputes tile s as its dummy partner;
+       // measured c3 621 -> 642 evals/s against one tile at a time, c4 unchanged)
+      const int r0 = 8 * (J + uw + (kW - 1) * s) + g, r1 = two ? r0 + 8 * (kW - 1) : r0;
+      const PointRec p0 = P[r0], p1 = P[r1];
+      a[0][0] = joint_entry<KIND>(p0, pc0, r0, c0, N, th, etab, pre);
+      a[0][1] = joint_entry<KIND>(p0, pc1, r0, c0 + 1, N, th, etab, pre);
+      a[1][0] = joint_entry<KIND>(p1, pc0, r1, c0, N, th, etab, pre);
+      a[1][1] = joint_entry<KIND>(p1, pc1, r1, c0 + 1, N, th, etab, pre);
     }
     const uint16_t* t0 = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (kW - 1) * s) * TI;
     if (two) {

@@ -35,9 +35,10 @@ namespace wk {
 
 using namespace tile;
 constexpr int kWMaxTI = 10;
-// Generated tiles in flight per lane: 2 (measured against 4: c5 m = 60 256.3 -> 269.8
-// evals/s, m = 30 unchanged — fewer live temporaries next to the register tiles).
-constexpr int kGenFly = 2;
+// Generated tiles in flight per lane: 1 (measured: 4 → 2 c5 m = 60 256.3 -> 269.8 evals/s,
+// m = 30 unchanged; 2 → 1 m = 30 690 -> 711, m = 60 262 -> 268 — fewer live temporaries next
+// to the register tiles, and one generation copy per panel).
+constexpr int kGenFly = 1;
 // The diagonal factorisation's pivot loop is a rolled loop here (factor_dist<1>): the
 // kernel is unrolled over its panels, so an unrolled pivot loop would put TI copies of
 // ~350 instructions into the code (TI = 7: 7.3k → 4.7k SASS instructions; measured
@@ -59,7 +60,9 @@ struct Layout {
   __host__ __device__ constexpr int bytes() const { return 8 * total; }
 };
 // Resident warps (= blocks) per SM the register budget targets (live tiles ≈ (TI/2)² + TI).
-__host__ __device__ constexpr int minb_for(int TI) { return TI >= 9 ? 12 : TI >= 8 ? 14 : TI >= 6 ? 16 : 20; }
+// (measured with one generated tile in flight: TI ≥ 9 at 14 instead of 12 blocks, c5 m = 60
+// 267.8 -> 277.3 evals/s; 16 for TI ≥ 9 or TI = 8, or 18 for TI 6-7: no gain or slower)
+__host__ __device__ constexpr int minb_for(int TI) { return TI >= 8 ? 14 : TI >= 6 ? 16 : 20; }
 
 template <int TI, int KIND>
 __global__ void __launch_bounds__(32, minb_for(TI)) bv_block_w_kernel(
