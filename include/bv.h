@@ -151,8 +151,11 @@ bv_status bv_owned_range(const bv_handle* h, int32_t* k_begin, int32_t* k_end);
 
 /* End-to-end variant (host observations in, ℓ out): copies y (n host
  * doubles, in global point-id order, all finite — else BV_EINVAL naming the
- * first non-finite entry) to the device inside the call, then evaluates.  Used
- * to time the whole path with host↔device traffic. */
+ * first non-finite entry, *loglik = −∞) to the device inside the call, then
+ * evaluates.  A non-finite y_i always makes its own block's term non-finite, so
+ * y is scanned on the host only when the evaluation fails (the precise error
+ * then replaces the block-level one); the success path never reads y on the
+ * host.  Used to time the whole path with host↔device traffic. */
 bv_status bv_loglik_host_y(bv_handle* h, const double* y, const double theta[3], double* loglik);
 
 /* ---- block-Vecchia prediction (Alg. 2; §2.3 :194-240) ----

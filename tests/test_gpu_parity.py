@@ -183,6 +183,14 @@ def test_determinism_and_host_y_path():
     y2 = p.y * 0.5
     assert bv.loglik_host_y(y2, theta) != a
     assert bv.loglik_host_y(p.y, theta) == a
+    # a non-finite y_i (checked on the host only after the evaluation failed): EINVAL naming it
+    for bad, i in ((float("nan"), 7), (float("inf"), p.n - 1), (-float("inf"), p.n // 2)):
+        y3 = p.y.copy()
+        y3[i] = bad
+        with pytest.raises(BVError) as e:
+            bv.loglik_host_y(y3, theta)
+        assert e.value.status == 2 and f"y[{i}]" in str(e.value)
+    assert bv.loglik_host_y(p.y, theta) == a
 
 
 def test_gpu_sigma2_and_length_scaling_exact():
