@@ -49,7 +49,6 @@ namespace v3 {
 // 4 warps per CTA (1 chain + 3 update): measured at c4, 5/6/8 warps per CTA gave
 // 187/180/166 evals/s against 197 (round 1).
 constexpr int kW = 4;  // warps per CTA: 1 chain warp + kW−1 update warps
-constexpr int kNT = kW * 32;
 #ifndef BV_REFINE_KAPPA
 #define BV_REFINE_KAPPA 100.0
 #endif
@@ -97,7 +96,7 @@ struct Layout {
     lrow = lfr + 128;        // (no row-major copy: panel solves are all DMMA)
     rinv = lrow;
     misc = lrow;             // [1] chain quad, [2] fail, [3] chain warp, [4] logdet, [5..7] update-warp quads
-    theta = misc + ((kW + 7) & ~1);  // Theta (≤ 20 doubles)
+    theta = misc + 16;  // Theta (≤ 20 doubles); misc holds 4 + KW ≤ 12 entries
     etab = theta + 20;       // 2^{−j/64}, j = 0..63 (exp_neg)
     slots = etab + 64;       // cap tiles
     tab = slots + 64 * cap;  // int16 slot table (TImax²)
@@ -222,7 +221,7 @@ __device__ __forceinline__ void u_place(double (&S)[MAXT][2], int s, double v0, 
       S[q][1] = v1;
     }
 }
-template <int MAXT, int KIND>
+template <int MAXT, int KIND, int KW>
 __device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const double* slots, const int16_t* tab, int TI,
                                          int J, int uw, int lane, const PointRec* P, int N, const Theta& th,
                                          const double* etab, const double* pre) {
@@ -236,16 +235,16 @@ __device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const dou
     double a[2][2];
     {  // both tiles' entries in flight (an odd tail recomputes tile s as its dummy partner;
        // measured c3 621 -> 642 evals/s against one tile at a time, c4 unchanged)
-      const int r0 = 8 * (J + uw + (kW - 1) * s) + g, r1 = two ? r0 + 8 * (kW - 1) : r0;
+      const int r0 = 8 * (J + uw + (KW - 1) * s) + g, r1 = two ? r0 + 8 * (KW - 1) : r0;
       const PointRec p0 = P[r0], p1 = P[r1];
       a[0][0] = joint_entry<KIND>(p0, pc0, r0, c0, N, th, etab, pre);
       a[0][1] = joint_entry<KIND>(p0, pc1, r0, c0 + 1, N, th, etab, pre);
       a[1][0] = joint_entry<KIND>(p1, pc0, r1, c0, N, th, etab, pre);
       a[1][1] = joint_entry<KIND>(p1, pc1, r1, c0 + 1, N, th, etab, pre);
     }
-    const uint16_t* t0 = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (kW - 1) * s) * TI;
+    const uint16_t* t0 = reinterpret_cast<const uint16_t*>(tab) + (J + uw + (KW - 1) * s) * TI;
     if (two) {
-      const uint16_t* t1 = t0 + (kW - 1) * TI;
+      const uint16_t* t1 = t0 + (KW - 1) * TI;
 #pragma unroll 2
       for (int K = 0; K < J; ++K) {
         const double2 b = lds2(slot_at(sl, tJ[K]));
@@ -286,8 +285,10 @@ constexpr int v3_minb(int maxt) { return maxt >= 16 ? 2 : maxt <= 5 ? BV_MINB5 :
 // scratch is gridDim × cap slots).  GS = "global slots".
 constexpr int kGsMaxT = 16;
 
-template <int MAXT, int KIND>
-__global__ void __launch_bounds__(kNT, v3_minb(MAXT))
+// KW: warps per CTA (1 chain + KW−1 update warps): 4, or 8 for the large joint sizes whose
+// tile slots leave room for only 2 CTAs per SM (host: v3_maxt_for).
+template <int MAXT, int KIND, int KW = kW>
+__global__ void __launch_bounds__(KW * 32, KW == kW ? v3_minb(MAXT) : 2)
 bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__ nbr,
                    const BlockDesc* __restrict__ desc, const int32_t* __restrict__ list,
                    const Theta* __restrict__ theta_dev, const int16_t* __restrict__ tabs,
@@ -325,7 +326,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   if (tid < (int)(sizeof(Theta) / 8))
     reinterpret_cast<double*>(ths)[tid] = reinterpret_cast<const double*>(theta_dev)[tid];
 #pragma unroll 1
-  for (int i = tid; i < 8 * TI; i += kNT) {
+  for (int i = tid; i < 8 * TI; i += (KW * 32)) {
     // padding rows/columns (i ≥ N, and the y row's own point): far-apart points, so every
     // padding entry off the diagonal is exactly 0 from Eq. (7) itself (x > 708 → 0) and no
     // per-entry validity select is needed (padding pivots are σ², exactly decoupled)
@@ -337,7 +338,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   {
     const int16_t* gt = tabs + tab_off[2 * TI + (TI - TJ)];
 #pragma unroll 1
-    for (int e = tid; e < TI * TI; e += kNT) tab[e] = gt[e];
+    for (int e = tid; e < TI * TI; e += (KW * 32)) tab[e] = gt[e];
   }
   if (tid < 4) misc[tid] = 0.0;
   __syncthreads();
@@ -347,7 +348,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   const Theta& th = *ths;
   // a3 panel 0: C(I,0) = A(I,0) for I ≥ 1 into slots; C(0,0) into dtile
 #pragma unroll 2
-  for (int e = tid; e < TI * 64; e += kNT) {
+  for (int e = tid; e < TI * 64; e += (KW * 32)) {
     const int I = e >> 6, r = 8 * I + ((e >> 3) & 7), c = e & 7;
     const double v = joint_entry<KIND>(P[r], P[c], r, c, N, th, etab, preb);
     if (I == 0) dtile[e] = v;
@@ -355,7 +356,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
   }
   __syncthreads();
   const int cw = (int)misc[3];
-  const int uw = (warp - cw + kW) % kW;  // 0 = chain warp, 1..kW−1 = update warps
+  const int uw = (warp - cw + KW) % KW;  // 0 = chain warp, 1..KW−1 = update warps
   const double pfloor = kPivotFloor * th.sigma2;
 
   if (uw == 0) {
@@ -394,8 +395,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       // U finished iteration J−1 (so it has consumed G, F, H of J−1: a named
       // barrier must not receive this warp's next arrival before its previous
       // phase completed)
-      if (J >= 1) bar_sync(kBarE, kNT);
-      bar_arrive(kBarG, kNT);
+      if (J >= 1) bar_sync(kBarE, (KW * 32));
+      bar_arrive(kBarG, (KW * 32));
       P3_ADD(1, t1);
       if (J + 1 >= TJ) {
         // last panel: when N is a multiple of 8 the y row sits alone in tile row
@@ -419,9 +420,9 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       tj[8 * g + 2 * ((2 * t + 1) & 3) + (t >> 1)] = x.y;
       P3_ADD(3, t3);
       P3_T(t4);
-      bar_sync(kBarH, kNT);  // the update warps published P(J+1,J+1)
+      bar_sync(kBarH, (KW * 32));  // the update warps published P(J+1,J+1)
       const double2 pp = lds2(ptile + 8 * g + 2 * t);  // read before F: U regenerates ptile after F
-      bar_arrive(kBarF, kNT);
+      bar_arrive(kBarF, (KW * 32));
       // C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ, straight into the next factorisation
       c0 = pp.x;
       c1 = pp.y;
@@ -448,15 +449,15 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         P3_T(u6);
         // a3 + a6: this warp's tiles of column J+1, generated into registers and reduced by
         // the panels K < J (exact tile count per warp: no predicated-off work)
-        const int ns = (TI - J - 1 - (uw - 1) + (kW - 2)) / (kW - 1);
-        u_column<MAXT, KIND>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb);
+        const int ns = (TI - J - 1 - (uw - 1) + (KW - 2)) / (KW - 1);
+        u_column<MAXT, KIND, KW>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb);
         // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp (warp 1 owns the tile)
         if (uw == 1) sts2(ptile + 8 * g + 2 * t, S[0][0], S[0][1]);
         P3_ADD(6, u6);
       }
       P3_T(u7);
-      bar_sync(kBarG, kNT);  // the chain warp published L_JJ
-      if (ahead) bar_arrive(kBarH, kNT);  // P(J+1,J+1) is in ptile
+      bar_sync(kBarG, (KW * 32));  // the chain warp published L_JJ
+      if (ahead) bar_arrive(kBarH, (KW * 32));  // P(J+1,J+1) is in ptile
       P3_ADD(7, u7);
       P3_T(u8);
       {
@@ -474,8 +475,8 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         const bool refine = mz * ml > kRefineKappa;
           // two tiles in flight: their DMMA / shared-memory round trips interleave
 #pragma unroll 1
-        for (int I = J + uw + (uw == 1 ? kW - 1 : 0); I < TI; I += 2 * (kW - 1)) {
-          const int I2 = I + kW - 1;
+        for (int I = J + uw + (uw == 1 ? KW - 1 : 0); I < TI; I += 2 * (KW - 1)) {
+          const int I2 = I + KW - 1;
           if (I2 < TI) {
             double* const tl[2] = {slot_at(slots, tabu[I * TI + J]), slot_at(slots, tabu[I2 * TI + J])};
             double2 d[2];
@@ -493,13 +494,13 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       // every L(I,J) is visible to all of them before the next GEMM)
       if (!ahead) continue;
       P3_T(u10);
-      bar_sync(kBarF, kNT);  // the chain warp published L(J+1,J)
+      bar_sync(kBarF, (KW * 32));  // the chain warp published L(J+1,J)
       P3_ADD(10, u10);
       P3_T(u11);
       const double2 b = lds2(slot_at(slots + 2 * lane, tabu[(J + 1) * TI + J]));
 #pragma unroll
       for (int s = 0; s < MAXT; ++s) {
-        const int I = J + uw + (kW - 1) * s;
+        const int I = J + uw + (KW - 1) * s;
         if (I < TI && I > J + 1) {  // the diagonal tile's last term is the chain warp's
           const double2 a = lds2(slot_at(slots + 2 * lane, tabu[I * TI + J]));
           dmma884(S[s][0], S[s][1], a.x, neg(b.x));
@@ -508,7 +509,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         }
       }
       __syncwarp();
-      bar_arrive(kBarE, kNT);  // iteration J done: C(I,J+1) stored, L(·,J) final
+      bar_arrive(kBarE, (KW * 32));  // iteration J done: C(I,J+1) stored, L(·,J) final
       P3_ADD(11, u11);
     }
     for (int o = 16; o > 0; o >>= 1) qd_u += __shfl_xor_sync(0xffffffffu, qd_u, o);
@@ -526,7 +527,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
     uint32_t c[6] = {0, 0, 0, 0, 0, 0};
     const double logdet = fail ? failed_d() : misc[4];
     double quad = misc[1];
-    for (int w = 1; w < kW; ++w) quad += misc[4 + w];  // fixed order: bitwise reproducible
+    for (int w = 1; w < KW; ++w) quad += misc[4 + w];  // fixed order: bitwise reproducible
     quad = fail ? 0.0 : quad;
     if (!fail) {
       const double tk = -0.5 * (quad + logdet + (double)l * kLn2Pi);
@@ -558,7 +559,22 @@ int debug_v3_cycles(unsigned long long* out, int reset) {
 #endif
 }
 
+// Instantiation for a tile-row count TI: MAXT (tiles per update warp) of the 4-warp kernel,
+// or 100 + MAXT of the 8-warp kernel (TI ≥ kKw8MinTI, shared-memory slots only).  From
+// TI ≈ 22 the tile slots leave room for only 2-3 CTAs per SM, and 7 update warps per block
+// recover the parallelism (measured: c5 m = 200 12.1 → 20.9 evals/s, c3 620 → 645 with
+// the threshold at 22; at 18 c3 572 and c5 m = 120 69 vs 80 — there 4-5 CTAs of 4 warps win).
+#ifndef BV_KW8_MIN_TI
+#define BV_KW8_MIN_TI 22
+#endif
+constexpr int kKw8MinTI = BV_KW8_MIN_TI;
 int v3_maxt_for(int TI) {
+  if (TI >= kKw8MinTI && TI <= 37) {
+    const int need8 = (TI - 1 + 6) / 7;
+    const int o8[] = {2, 3, 4, 5, 6};
+    for (int o : o8)
+      if (o >= need8) return 100 + o;
+  }
   const int need = (TI - 1 + (v3::kW - 2)) / (v3::kW - 1);  // panel J+1 tiles I ≥ J+1 over the update warps
   const int opts[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16, 20};
   for (int o : opts)
@@ -566,22 +582,25 @@ int v3_maxt_for(int TI) {
   return -1;
 }
 
-bool v3_global_slots(int TI) { return v3_maxt_for(TI) >= v3::kGsMaxT; }
+bool v3_global_slots(int TI) {
+  const int mt = v3_maxt_for(TI);
+  return mt >= v3::kGsMaxT && mt < 100;
+}
 
 size_t v3_smem_bytes(int TImax, int cap) {
   const size_t b = (size_t)v3::Layout(TImax, v3_global_slots(TImax) ? 0 : cap).total_bytes;
   return b;
 }
 
-template <int MAXT>
+template <int MAXT, int KW = v3::kW>
 static cudaError_t v3_prep(size_t smem) {
   cudaError_t e = cudaSuccess;
   for (int k = 0; k < 5 && e == cudaSuccess; ++k) {
-    const void* f = k == 0 ? (const void*)v3::bv_block_v3_kernel<MAXT, 0>
-                  : k == 1 ? (const void*)v3::bv_block_v3_kernel<MAXT, 1>
-                  : k == 2 ? (const void*)v3::bv_block_v3_kernel<MAXT, 2>
-                  : k == 3 ? (const void*)v3::bv_block_v3_kernel<MAXT, 3>
-                           : (const void*)v3::bv_block_v3_kernel<MAXT, v3::kPre>;
+    const void* f = k == 0 ? (const void*)v3::bv_block_v3_kernel<MAXT, 0, KW>
+                  : k == 1 ? (const void*)v3::bv_block_v3_kernel<MAXT, 1, KW>
+                  : k == 2 ? (const void*)v3::bv_block_v3_kernel<MAXT, 2, KW>
+                  : k == 3 ? (const void*)v3::bv_block_v3_kernel<MAXT, 3, KW>
+                           : (const void*)v3::bv_block_v3_kernel<MAXT, v3::kPre, KW>;
     e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   return e;
@@ -600,17 +619,24 @@ cudaError_t prepare_block_v3(size_t max_smem) {
   if (e == cudaSuccess) e = v3_prep<12>(max_smem);
   if (e == cudaSuccess) e = v3_prep<16>(max_smem);
   if (e == cudaSuccess) e = v3_prep<20>(max_smem);
+  if (kKw8MinTI <= 37) {
+    if (e == cudaSuccess) e = v3_prep<2, 8>(max_smem);
+    if (e == cudaSuccess) e = v3_prep<3, 8>(max_smem);
+    if (e == cudaSuccess) e = v3_prep<4, 8>(max_smem);
+    if (e == cudaSuccess) e = v3_prep<5, 8>(max_smem);
+    if (e == cudaSuccess) e = v3_prep<6, 8>(max_smem);
+  }
   return e;
 }
 
-template <int MAXT>
+template <int MAXT, int KW = v3::kW>
 static void v3_launch_kind(int kind, int nblocks, size_t smem, cudaStream_t s, const PointRec* pts,
                            const int32_t* nbr, const BlockDesc* desc, const int32_t* list, const Theta* th,
                            const int16_t* tabs, const int32_t* tab_off, const double* etab, int TImax, int cap,
                            double* u, double* d, unsigned long long* acc, int k_begin, double* gslots, int grid,
                            const double* pre, const int64_t* pre_off, double jit) {
 #define BV_K(KD)                                                                                             \
-  v3::bv_block_v3_kernel<MAXT, KD><<<grid, v3::kNT, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, \
+  v3::bv_block_v3_kernel<MAXT, KD, KW><<<grid, KW * 32, smem, s>>>(pts, nbr, desc, list, th, tabs, tab_off, etab, \
                                                                TImax, cap, u, d, acc, k_begin, gslots, nblocks, \
                                                                pre, pre_off, jit)
   switch (kind) {
@@ -639,6 +665,13 @@ cudaError_t launch_block_v3(int kind, int nblocks, int TImax, int cap, cudaStrea
     break;
     BV_MT(1) BV_MT(2) BV_MT(3) BV_MT(4) BV_MT(5) BV_MT(6) BV_MT(8) BV_MT(10) BV_MT(12) BV_MT(16) BV_MT(20)
 #undef BV_MT
+#define BV_MT8(MT)                                                                                           \
+  case 100 + MT:                                                                                             \
+    v3_launch_kind<MT, 8>(kind, nblocks, smem, s, pts, nbr, desc, list, th, tabs, tab_off, etab, TImax, cap, u, \
+                          d, acc, k_begin, gslots, grid, pre, pre_off, jit);                                 \
+    break;
+    BV_MT8(2) BV_MT8(3) BV_MT8(4) BV_MT8(5) BV_MT8(6)
+#undef BV_MT8
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
