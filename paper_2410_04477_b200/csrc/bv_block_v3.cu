@@ -224,7 +224,7 @@ __device__ __forceinline__ void u_place(double (&S)[MAXT][2], int s, double v0, 
 template <int MAXT, int KIND, int KW>
 __device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const double* slots, const int16_t* tab, int TI,
                                          int J, int uw, int lane, const PointRec* P, int N, const Theta& th,
-                                         const double* etab, const double* pre) {
+                                         const double* etab, const double* pre, double* ptile) {
   const int g = lane >> 2, t = lane & 3, c0 = 8 * (J + 1) + 2 * t;
   const PointRec pc0 = P[c0], pc1 = P[c0 + 1];
   const double* sl = slots + 2 * lane;
@@ -267,6 +267,12 @@ __device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const dou
       }
     }
     u_place(S, s, a[0][0], a[0][1]);
+#ifdef BV_EARLY_P
+    if (s == 0 && ptile) {  // warp 1: P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ done — hand it over now
+      sts2(ptile + 8 * g + 2 * t, a[0][0], a[0][1]);
+      bar_arrive(kBarH, 64);  // the chain warp and warp 1 only
+    }
+#endif
   }
 }
 
@@ -285,10 +291,13 @@ constexpr int v3_minb(int maxt) { return maxt >= 16 ? 2 : maxt <= 5 ? BV_MINB5 :
 // scratch is gridDim × cap slots).  GS = "global slots".
 constexpr int kGsMaxT = 16;
 
+#ifndef BV_KW8_MINB3
+#define BV_KW8_MINB3 3  // 8-warp CTAs per SM targeted for MAXT ≤ 3 (TI ≤ 22; shared memory admits 3)
+#endif
 // KW: warps per CTA (1 chain + KW−1 update warps): 4, or 8 for the large joint sizes whose
 // tile slots leave room for only 2 CTAs per SM (host: v3_maxt_for).
 template <int MAXT, int KIND, int KW = kW>
-__global__ void __launch_bounds__(KW * 32, KW == kW ? v3_minb(MAXT) : 2)
+__global__ void __launch_bounds__(KW * 32, KW == kW ? v3_minb(MAXT) : (MAXT <= 3 ? BV_KW8_MINB3 : 2))
 bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__ nbr,
                    const BlockDesc* __restrict__ desc, const int32_t* __restrict__ list,
                    const Theta* __restrict__ theta_dev, const int16_t* __restrict__ tabs,
@@ -420,7 +429,11 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       tj[8 * g + 2 * ((2 * t + 1) & 3) + (t >> 1)] = x.y;
       P3_ADD(3, t3);
       P3_T(t4);
+#ifdef BV_EARLY_P
+      bar_sync(kBarH, 64);  // update warp 1 published P(J+1,J+1)
+#else
       bar_sync(kBarH, (KW * 32));  // the update warps published P(J+1,J+1)
+#endif
       const double2 pp = lds2(ptile + 8 * g + 2 * t);  // read before F: U regenerates ptile after F
       bar_arrive(kBarF, (KW * 32));
       // C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ, straight into the next factorisation
@@ -450,14 +463,20 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         // a3 + a6: this warp's tiles of column J+1, generated into registers and reduced by
         // the panels K < J (exact tile count per warp: no predicated-off work)
         const int ns = (TI - J - 1 - (uw - 1) + (KW - 2)) / (KW - 1);
-        u_column<MAXT, KIND, KW>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb);
+#ifdef BV_EARLY_P
+        u_column<MAXT, KIND, KW>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb, uw == 1 ? ptile : nullptr);
+#else
+        u_column<MAXT, KIND, KW>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb, nullptr);
         // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp (warp 1 owns the tile)
         if (uw == 1) sts2(ptile + 8 * g + 2 * t, S[0][0], S[0][1]);
+#endif
         P3_ADD(6, u6);
       }
       P3_T(u7);
       bar_sync(kBarG, (KW * 32));  // the chain warp published L_JJ
+#ifndef BV_EARLY_P
       if (ahead) bar_arrive(kBarH, (KW * 32));  // P(J+1,J+1) is in ptile
+#endif
       P3_ADD(7, u7);
       P3_T(u8);
       {
@@ -561,11 +580,12 @@ int debug_v3_cycles(unsigned long long* out, int reset) {
 
 // Instantiation for a tile-row count TI: MAXT (tiles per update warp) of the 4-warp kernel,
 // or 100 + MAXT of the 8-warp kernel (TI ≥ kKw8MinTI, shared-memory slots only).  From
-// TI ≈ 22 the tile slots leave room for only 2-3 CTAs per SM, and 7 update warps per block
+// TI ≈ 20 the tile slots leave room for only 2-3 CTAs per SM, and 7 update warps per block
 // recover the parallelism (measured: c5 m = 200 12.1 → 20.9 evals/s, c3 620 → 645 with
-// the threshold at 22; at 18 c3 572 and c5 m = 120 69 vs 80 — there 4-5 CTAs of 4 warps win).
+// the threshold at 22 and 2 CTAs per SM; threshold 20 with 3 CTAs per SM for TI ≤ 22: c3 622
+// → 640, m = 120 78.5 → 79.4; at 17-18 c3 and m = 120 lose — 4-5 CTAs of 4 warps win there).
 #ifndef BV_KW8_MIN_TI
-#define BV_KW8_MIN_TI 22
+#define BV_KW8_MIN_TI 20
 #endif
 constexpr int kKw8MinTI = BV_KW8_MIN_TI;
 int v3_maxt_for(int TI) {
