@@ -224,7 +224,7 @@ __device__ __forceinline__ void u_place(double (&S)[MAXT][2], int s, double v0, 
 template <int MAXT, int KIND, int KW>
 __device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const double* slots, const int16_t* tab, int TI,
                                          int J, int uw, int lane, const PointRec* P, int N, const Theta& th,
-                                         const double* etab, const double* pre, double* ptile) {
+                                         const double* etab, const double* pre) {
   const int g = lane >> 2, t = lane & 3, c0 = 8 * (J + 1) + 2 * t;
   const PointRec pc0 = P[c0], pc1 = P[c0 + 1];
   const double* sl = slots + 2 * lane;
@@ -267,12 +267,6 @@ __device__ __forceinline__ void u_column(double (&S)[MAXT][2], int ns, const dou
       }
     }
     u_place(S, s, a[0][0], a[0][1]);
-#ifdef BV_EARLY_P
-    if (s == 0 && ptile) {  // warp 1: P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ done — hand it over now
-      sts2(ptile + 8 * g + 2 * t, a[0][0], a[0][1]);
-      bar_arrive(kBarH, 64);  // the chain warp and warp 1 only
-    }
-#endif
   }
 }
 
@@ -429,11 +423,7 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
       tj[8 * g + 2 * ((2 * t + 1) & 3) + (t >> 1)] = x.y;
       P3_ADD(3, t3);
       P3_T(t4);
-#ifdef BV_EARLY_P
-      bar_sync(kBarH, 64);  // update warp 1 published P(J+1,J+1)
-#else
       bar_sync(kBarH, (KW * 32));  // the update warps published P(J+1,J+1)
-#endif
       const double2 pp = lds2(ptile + 8 * g + 2 * t);  // read before F: U regenerates ptile after F
       bar_arrive(kBarF, (KW * 32));
       // C(J+1,J+1) = P − L(J+1,J) L(J+1,J)ᵀ, straight into the next factorisation
@@ -463,20 +453,14 @@ bv_block_v3_kernel(const PointRec* __restrict__ pts, const int32_t* __restrict__
         // a3 + a6: this warp's tiles of column J+1, generated into registers and reduced by
         // the panels K < J (exact tile count per warp: no predicated-off work)
         const int ns = (TI - J - 1 - (uw - 1) + (KW - 2)) / (KW - 1);
-#ifdef BV_EARLY_P
-        u_column<MAXT, KIND, KW>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb, uw == 1 ? ptile : nullptr);
-#else
-        u_column<MAXT, KIND, KW>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb, nullptr);
+        u_column<MAXT, KIND, KW>(S, ns, slots, tab, TI, J, uw, lane, P, N, th, etab, preb);
         // P(J+1,J+1) = A − Σ_{K<J} L(J+1,K) L(J+1,K)ᵀ for the chain warp (warp 1 owns the tile)
         if (uw == 1) sts2(ptile + 8 * g + 2 * t, S[0][0], S[0][1]);
-#endif
         P3_ADD(6, u6);
       }
       P3_T(u7);
       bar_sync(kBarG, (KW * 32));  // the chain warp published L_JJ
-#ifndef BV_EARLY_P
       if (ahead) bar_arrive(kBarH, (KW * 32));  // P(J+1,J+1) is in ptile
-#endif
       P3_ADD(7, u7);
       P3_T(u8);
       {
