@@ -1,14 +1,14 @@
-// bv_block_v3.cu — the large-block kernel (joint sizes N ≥ 64): one block per CTA,
-// warp-specialised.
+// bv_block_v3.cu — the large-block kernel (joint sizes N ≥ 80; smaller ones go to the
+// warp-per-block kernel, bv_block_w.cu): one block per CTA, warp-specialised.
 //
 // One Cholesky of the augmented joint matrix [[Σcon, Σcross, y_NN],[Σcrossᵀ, Σlk,
 // y_B]] (Alg. 1 l.10-29, fused as in DESIGN.md §4), left-looking
 // over 8-wide column panels, FP64 MMA (DMMA.8x8x4) for every tile product, Matérn
 // generated on the fly.  A dedicated chain warp factors the diagonal tiles and
-// hands each panel to the three update warps through named barriers
-// (bar.arrive / bar.sync), one panel ahead:
+// hands each panel to the update warps (3, or 7 from 20 tile rows: KW) through named
+// barriers (bar.arrive / bar.sync), one panel ahead:
 //
-//  chain warp, iteration J:                    update warps (96 threads), iteration J:
+//  chain warp, iteration J:                    update warps, iteration J:
 //    factor C(J,J) across its lanes → publish    generate A(I,J+1) for their tiles I ≥ J+1
 //      L_JJ and L_JJ⁻¹ (tile::factor_dist)         straight into MMA accumulators, then
 //    sync  E  (updates of iteration J−1 done)      S ← S − L(I,K) L(J+1,K)ᵀ, K = 0..J−1
@@ -46,8 +46,9 @@ namespace v3 {
 // with unchanged parity statistics (gpurun_out/abk: every c1-c4 case, same strict /
 // κ-branch / replica counts within noise); 1000 fails two c4 blocks; no refinement at
 // all fails c3 (26 blocks) — the chain warp's own solve always refines.
-// 4 warps per CTA (1 chain + 3 update): measured at c4, 5/6/8 warps per CTA gave
-// 187/180/166 evals/s against 197 (round 1).
+// 4 warps per CTA (1 chain + 3 update) up to 19 tile rows: measured at c4, 5/6/8 warps
+// per CTA gave 187/180/166 evals/s against 197 (round 1), and 8 warps from 14 tile rows
+// 151-185 against 226 (round 2); 8 from 20 tile rows: see v3_maxt_for.
 constexpr int kW = 4;  // warps per CTA: 1 chain warp + kW−1 update warps
 #ifndef BV_REFINE_KAPPA
 #define BV_REFINE_KAPPA 100.0
