@@ -1,5 +1,7 @@
-// bv_block_w.cu — the small-block kernel: ONE WARP per block, the whole joint
-// matrix in REGISTERS (joint sizes N ≤ 8·TI − 1, TI ≤ kWMaxTI), many blocks per SM.
+// bv_block_w.cu — the warp-per-block kernel: ONE WARP per block, the whole joint
+// matrix in REGISTERS (joint sizes N ≤ 8·TI − 1, TI ≤ kWMaxTI = 16), many blocks per SM.
+// The host sends every bucket with TI ≤ 12 here, and the buckets with TI ≤ 16 that hold at
+// least 2,048 blocks (bv_host.cpp: one warp per block needs a full wave of warps).
 //
 // Same mathematics as the large-block kernel (Alg. 1 l.10-29, PAPER.md:593-632,
 // fused into one Cholesky of the joint matrix with the y row appended, DESIGN.md
@@ -34,7 +36,7 @@ namespace bv {
 namespace wk {
 
 using namespace tile;
-constexpr int kWMaxTI = 10;
+constexpr int kWMaxTI = 16;
 // Generated tiles in flight per lane: 1 (measured: 4 → 2 c5 m = 60 256.3 -> 269.8 evals/s,
 // m = 30 unchanged; 2 → 1 m = 30 690 -> 711, m = 60 262 -> 268 — fewer live temporaries next
 // to the register tiles, and one generation copy per panel).
@@ -62,7 +64,12 @@ struct Layout {
 // Resident warps (= blocks) per SM the register budget targets (live tiles ≈ (TI/2)² + TI).
 // (measured with one generated tile in flight: TI ≥ 9 at 14 instead of 12 blocks, c5 m = 60
 // 267.8 -> 277.3 evals/s; 16 for TI ≥ 9 or TI = 8, or 18 for TI 6-7: no gain or slower)
-__host__ __device__ constexpr int minb_for(int TI) { return TI >= 8 ? 14 : TI >= 6 ? 16 : 20; }
+// (TI 11-16 for the large buckets: TI = 16 needs the full 255 registers and
+// still spills ~400 B per thread; capping it lower spills more, and it measured faster than
+// the CTA kernel anyway)
+__host__ __device__ constexpr int minb_for(int TI) {
+  return TI >= 15 ? 8 : TI >= 13 ? 10 : TI >= 11 ? 12 : TI >= 8 ? 14 : TI >= 6 ? 16 : 20;
+}
 
 template <int TI, int KIND>
 __global__ void __launch_bounds__(32, minb_for(TI)) bv_block_w_kernel(
@@ -205,7 +212,7 @@ static cudaError_t w_launch_ti(int kind, int nblocks, cudaStream_t s, const Poin
 cudaError_t prepare_block_w() {
   cudaError_t e = cudaSuccess;
 #define BV_P(T) if (e == cudaSuccess) e = w_prep_ti<T>();
-  BV_P(1) BV_P(2) BV_P(3) BV_P(4) BV_P(5) BV_P(6) BV_P(7) BV_P(8) BV_P(9) BV_P(10)
+  BV_P(1) BV_P(2) BV_P(3) BV_P(4) BV_P(5) BV_P(6) BV_P(7) BV_P(8) BV_P(9) BV_P(10) BV_P(11) BV_P(12) BV_P(13) BV_P(14) BV_P(15) BV_P(16)
 #undef BV_P
   return e;
 }
@@ -219,7 +226,7 @@ cudaError_t launch_block_w(int kind, int nblocks, int TI, cudaStream_t s, const 
 #define BV_T(T)                                                                                                  \
   case T:                                                                                                        \
     return w_launch_ti<T>(kind, nblocks, s, pts, nbr, desc, list, th, etab, u, d, acc, k_begin, pre, pre_off, jit);
-    BV_T(1) BV_T(2) BV_T(3) BV_T(4) BV_T(5) BV_T(6) BV_T(7) BV_T(8) BV_T(9) BV_T(10)
+    BV_T(1) BV_T(2) BV_T(3) BV_T(4) BV_T(5) BV_T(6) BV_T(7) BV_T(8) BV_T(9) BV_T(10) BV_T(11) BV_T(12) BV_T(13) BV_T(14) BV_T(15) BV_T(16)
 #undef BV_T
     default: return cudaErrorInvalidValue;
   }

@@ -150,6 +150,7 @@ struct bv_handle {
   bool local = false;                      // test-only rank-local handle (bv_setup_rank_local): no communicator
   int wmax = 0;                            // largest TI run by the warp-per-block kernel
   std::vector<int> cap_of;                 // v3 slot capacity by TI
+  std::vector<int> kern_of;                // kernel of each TI's bucket (jitter retries use the same)
   std::vector<size_t> gsoff_of;            // v3 global-slot scratch offset by TI (TI > 37)
   bv::Theta* h_theta = nullptr;            // pinned
   unsigned long long* h_acc = nullptr;     // pinned
@@ -489,8 +490,17 @@ static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world
   // BV_WMAX=t are A/B switches only.
   const char* kenv = std::getenv("BV_KERNEL");
   const bool force_v3 = kenv && std::string(kenv) == "v3";
+  // Up to wmax tile rows every bucket goes to the warp-per-block kernel; up to wbig only the
+  // buckets with at least wbig_min blocks in the whole plan (one warp per block: a small
+  // bucket of large blocks would leave its last blocks' single warps as the tail — measured
+  // c5 m = 60: its 1,175 TI = 13 blocks 306 → 291 evals/s on the warp kernel; c4: its 21,460
+  // TI = 15 and 19,044 TI = 16 blocks 229 → 247 → 252 on it; TI 17 neutral, TI 18 slower).
   const char* wenv = std::getenv("BV_WMAX");
-  const int wmax = force_v3 ? 0 : std::max(0, std::min(bv::w_max_ti(), wenv ? std::atoi(wenv) : 10));
+  const char* wbenv = std::getenv("BV_WBIG");
+  const char* wmenv = std::getenv("BV_WBIG_MIN");
+  const int wmax = force_v3 ? 0 : std::max(0, std::min(bv::w_max_ti(), wenv ? std::atoi(wenv) : 12));
+  const int wbig = force_v3 ? 0 : std::max(wmax, std::min(bv::w_max_ti(), wbenv ? std::atoi(wbenv) : 16));
+  const int wbig_min = wmenv ? std::atoi(wmenv) : 2048;
   const int Nlimit = [&] {
     int N = 8;
     SlotTables st;
@@ -592,6 +602,15 @@ static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world
     if (Nq(a) != Nq(b)) return Nq(a) > Nq(b);
     return a < b;
   });
+  // bucket sizes over the WHOLE plan (not this rank's range): the kernel of a tile-row count
+  // is a property of the plan, so every world size runs every block on the same kernel and
+  // ℓ is bitwise the same for any G (§6)
+  std::vector<int64_t> glob_count(64 + 2, 0);
+  for (int32_t k = 0; k < bc; ++k) {
+    const bool cv = cv_ok && L[k] == 1 && M[k] <= 31;
+    const int TI = (L[k] + M[k] + 8) >> 3;
+    if (!cv && TI < (int)glob_count.size()) ++glob_count[(size_t)TI];
+  }
   SlotTables slot_tables;
   int TImax_all = 1;
   for (int32_t q = 0; q < h->nq; ++q) TImax_all = std::max(TImax_all, (Nq(q) + 8) >> 3);
@@ -612,7 +631,7 @@ static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world
     Bucket bk{TI, j - i, i, TI ? slot_tables.cap[TI] : 0};
     if (TI == 0) {
       bk.kern = kKernCV;
-    } else if (TI <= wmax) {
+    } else if (TI <= wmax || (TI <= wbig && glob_count[(size_t)TI] >= wbig_min)) {
       bk.kern = kKernW;
       any_w = true;
     } else {
@@ -625,6 +644,10 @@ static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world
       max_smem = std::max(max_smem, bv::v3_smem_bytes(TI, slot_tables.cap[TI]));
     }
     h->buckets.push_back(bk);
+    if (TI > 0) {
+      if ((int)h->kern_of.size() <= TI) h->kern_of.resize((size_t)TI + 1, -1);
+      h->kern_of[(size_t)TI] = bk.kern;
+    }
     i = j;
   }
 
@@ -794,7 +817,11 @@ static bv_status jitter_retry(bv_handle* h, const unsigned long long* acc, doubl
         while (j < R.size() && ti(R[j]) == ti(R[i])) ++j;
         const int TI = ti(R[i]);
         Bucket b{TI, (int)(j - i), 0, h->cap_of[(size_t)TI]};
-        b.kern = TI <= h->wmax ? kKernW : kKernV3;
+        // the kernel this TI's bucket runs in the evaluation (classic-Vecchia positions, which
+        // have no block-kernel bucket, by the size rule alone)
+        b.kern = (size_t)TI < h->kern_of.size() && h->kern_of[(size_t)TI] >= 0 ? h->kern_of[(size_t)TI]
+                 : TI <= h->wmax                                            ? kKernW
+                                                                            : kKernV3;
         b.gs_off = h->gsoff_of[(size_t)TI];
         BV_CUDA(h, launch_bucket(h, b, kind, h->stream, h->d_jlist + i, b.count, h->d_jacc, kSched[e] * s2));
         i = j;
