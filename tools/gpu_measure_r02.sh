@@ -23,7 +23,18 @@ for spec in "c4 2" "c5 2 30" "c3 2"; do
   timeout 900 ncu --metrics $M --clock-control none --csv --log-file $O/counts_$tag.csv python tools/prof_run.py $spec > $O/ncu_$tag.log 2>&1
 done
 timeout 300 python tools/prof_run.py c4 1 > $O/plain_full.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:v3_kernel<\(int\)5" -c 1 -o $O/full_c4 -f python tools/prof_run.py c4 1 > $O/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:w_kernel<\(int\)16" -c 1 -o $O/full_c4 -f python tools/prof_run.py c4 1 > $O/ncu_full.log 2>&1
+timeout 300 python tools/prof_run.py c3 1 > $O/plain_full_c3.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:v3_kernel<\(int\)6" -c 1 -o $O/full_c3 -f python tools/prof_run.py c3 1 > $O/ncu_full_c3.log 2>&1
 timeout 300 python tools/prof_run.py c5 1 30 > $O/plain_full_w.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:w_kernel<\(int\)7" -c 1 -o $O/full_c5w -f python tools/prof_run.py c5 1 30 > $O/ncu_full_w.log 2>&1
+# summaries on the box (the .ncu-rep files are too large to bring back): tracked markdown + raw csv
+for spec in "full_c4 r02 dominant_c4_launch" "full_c3 r02_c3 dominant_c3_launch" "full_c5w r02_c5w dominant_c5_m30_launch"; do
+  set -- $spec
+  if [ -f $O/$1.ncu-rep ]; then
+    python tools/ncu_summary.py full $O/$1.ncu-rep $2 "$3" > /dev/null 2>&1 && cp profiles/ncu_$2.md $O/
+    ncu -i $O/$1.ncu-rep --page raw --csv > $O/raw_$1.csv 2>/dev/null
+    rm -f $O/$1.ncu-rep
+  fi
+done
 echo done > $O/done
