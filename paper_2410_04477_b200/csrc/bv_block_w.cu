@@ -1,7 +1,7 @@
 // bv_block_w.cu — the warp-per-block kernel: ONE WARP per block, the whole joint
 // matrix in REGISTERS (joint sizes N ≤ 8·TI − 1, TI ≤ kWMaxTI = 16), many blocks per SM.
-// The host sends every bucket with TI ≤ 12 here, and the buckets with TI ≤ 16 that hold at
-// least 2,048 blocks (bv_host.cpp: one warp per block needs a full wave of warps).
+// The host sends every bucket with TI ≤ 10 here, and the buckets with TI ≤ 16 that hold at
+// least 2,048 blocks of the plan (bv_host.cpp: one warp per block needs a full wave of warps).
 //
 // Same mathematics as the large-block kernel (Alg. 1 l.10-29, PAPER.md:593-632,
 // fused into one Cholesky of the joint matrix with the y row appended, DESIGN.md

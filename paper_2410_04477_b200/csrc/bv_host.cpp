@@ -490,7 +490,7 @@ static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world
   // BV_WMAX=t are A/B switches only.
   const char* kenv = std::getenv("BV_KERNEL");
   const bool force_v3 = kenv && std::string(kenv) == "v3";
-  // Up to wmax tile rows every bucket goes to the warp-per-block kernel; up to wbig only the
+  // Up to wmax (10) tile rows every bucket goes to the warp-per-block kernel; up to wbig only the
   // buckets with at least wbig_min blocks in the whole plan (one warp per block: a small
   // bucket of large blocks would leave its last blocks' single warps as the tail — measured
   // c5 m = 60: its 1,175 TI = 13 blocks 306 → 291 evals/s on the warp kernel; c4: its 21,460
@@ -498,7 +498,7 @@ static bv_status setup_impl(const bv_plan* plan, int device, int rank, int world
   const char* wenv = std::getenv("BV_WMAX");
   const char* wbenv = std::getenv("BV_WBIG");
   const char* wmenv = std::getenv("BV_WBIG_MIN");
-  const int wmax = force_v3 ? 0 : std::max(0, std::min(bv::w_max_ti(), wenv ? std::atoi(wenv) : 12));
+  const int wmax = force_v3 ? 0 : std::max(0, std::min(bv::w_max_ti(), wenv ? std::atoi(wenv) : 10));
   const int wbig = force_v3 ? 0 : std::max(wmax, std::min(bv::w_max_ti(), wbenv ? std::atoi(wbenv) : 16));
   const int wbig_min = wmenv ? std::atoi(wmenv) : 2048;
   const int Nlimit = [&] {
